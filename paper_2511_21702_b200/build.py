@@ -1,0 +1,78 @@
+"""In-tree build of the sm_100a extension (and the oracle's C checker).
+
+`python -m paper_2511_21702_b200.build` or `__graft_entry__.build()`.
+The .so lands in paper_2511_21702_b200/_build/ (git-ignored, shipped to the
+GPU box with the gpurun snapshot).
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT_DIR = os.path.join(HERE, "_build")
+OUT = os.path.join(OUT_DIR, "libcsvd_b200.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false",            # belt and braces: the kernels use __dmul_rn/__dadd_rn anyway
+    "-Xcompiler", "-fPIC", "-shared",
+    "-Xptxas", "-v",
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def sources():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))] + \
+        [os.path.join(ROOT, "include", "csvd_b200.h")]
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    return all(os.path.getmtime(s) <= t for s in sources())
+
+
+def build_extension(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    os.makedirs(OUT_DIR, exist_ok=True)
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", os.path.join(CSRC, "csvd_b200.cu")]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    log = os.path.join(OUT_DIR, "ptxas.log")
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stderr)
+        raise RuntimeError(f"nvcc failed (see {log})")
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print(proc.stderr)
+    return OUT
+
+
+def build_oracle() -> str:
+    """Build the oracle's C restatement (test infrastructure, not the product)."""
+    odir = os.path.join(ROOT, "oracle")
+    proc = subprocess.run(["make", "-s", "-C", odir, "CC=gcc"], capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError("oracle build failed: " + proc.stderr)
+    return os.path.join(odir, "_build", "libcsvd_oracle.so")
+
+
+if __name__ == "__main__":
+    print(build_extension(force="--force" in sys.argv, verbose=True))
+    print(build_oracle())

@@ -1,0 +1,379 @@
+"""Python mirror of the reference's hot-path API, executed on the B200.
+
+Drop-in replacements (same signatures, same outputs, same errors):
+
+* `decode_step(table, index, h, cfg, k_max=None)`            decode.py:312-343
+* `decode_step_batchselect(table, index, h, cfg, k_max=None)` decode.py:362-382
+* `cluster_bounds(index, h, query_norm=None, slack_mode="none")` bounds.py:178-184
+* `dense_logits(table, h)`                                   oracle.py:33-41
+
+Every call runs the CUDA-graph step of `csrc/csvd_b200.cu` through the C ABI
+(`include/csvd_b200.h`); there is no CPU fallback.  The per-step SHA-256
+table fingerprint of the reference (`_check_table_index`, decode.py:142-144)
+is evaluated once, when a (table, index) pair is first uploaded (`prepare`),
+and the device context is cached for that pair.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .types import (
+    BoundVector,
+    CertStatus,
+    ConfigError,
+    DecodeOutcome,
+    DenseResult,
+    StepMetrics,
+    bf16_bits_to_f32,
+    resolved_k_max,
+    validate_config,
+)
+from .workload import table_fingerprint
+
+NEG_INF = float("-inf")
+
+
+class CsvdError(RuntimeError):
+    pass
+
+
+def _raise(code: int, msg: str):
+    if code == _lib.E_CONFIG:
+        raise ConfigError(msg)
+    if code in (_lib.E_DIM, _lib.E_VALUE):
+        raise ValueError(msg)
+    raise CsvdError(f"csvd_b200 error {code}: {msg}")
+
+
+def _ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+class DeviceIndex:
+    """A (table, index) pair resident on one B200 (the `prepare` step).
+
+    Layout in HBM: W permuted to cluster order (each cluster a contiguous row
+    range, fp32 or bf16), bias permuted (f32), f64 centroids, per-cluster
+    radius / max-bias / log-size, and static per-step workspaces sized for the
+    worst case (|S| <= V).  See DESIGN.md §3.
+    """
+
+    def __init__(self, table, index, device: int = 0, check_fingerprint: bool = True,
+                 weights_required: bool = True):
+        lib = _lib.load()
+        if table is not None and check_fingerprint:
+            if index.fingerprint != table_fingerprint(table):
+                raise ConfigError("index fingerprint does not match table")
+        self.device = device
+        self.mode = index.mode
+        self.V = int(index.vocab_size)
+        self.d = int(index.hidden_dim)
+        self.C = int(index.n_clusters)
+        self.bounds_dim = self.d + (1 if self.mode == "bias_augmented" else 0)
+        if self.mode not in _lib.MODE_CODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+        keep = []
+
+        def c(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a
+
+        td = _lib.TableDesc()
+        td.vocab_size = self.V
+        td.hidden_dim = self.d
+        if table is not None:
+            if table.vocab_size != self.V or table.hidden_dim != self.d:
+                raise ValueError("table / index shape mismatch")
+            w = table.weights
+            if w.dtype == np.uint16:
+                td.w_dtype = _lib.W_BF16
+                wa = c(w, np.uint16)
+            else:
+                td.w_dtype = _lib.W_F32
+                wa = w if w.dtype == np.float32 else w.astype(np.float32)
+                if w.dtype == np.float64 and not np.array_equal(wa.astype(np.float64), w):
+                    raise ValueError("float64 weights must be float32-exact (tensor_io.py:156)")
+                wa = c(wa, np.float32)
+            td.weights = wa.ctypes.data
+            b32 = c(np.asarray(table.bias, dtype=np.float32), np.float32)
+            td.bias = b32.ctypes.data
+            self.w_dtype = "bf16" if td.w_dtype == _lib.W_BF16 else "f32"
+        else:
+            td.w_dtype = _lib.W_F32
+            td.weights = None
+            td.bias = None
+            self.w_dtype = None
+        ix = _lib.IndexDesc()
+        ix.n_clusters = self.C
+        ix.mode = _lib.MODE_CODES[self.mode]
+        ix.perm = c(index.perm, np.int64).ctypes.data
+        ix.starts = c(index.starts, np.int64).ctypes.data
+        ix.sizes = c(index.sizes, np.int64).ctypes.data
+        cent = c(index.centroids, np.float64)
+        if cent.shape != (self.C, self.bounds_dim):
+            raise ValueError("centroid shape mismatch")
+        ix.centroids = cent.ctypes.data
+        ix.radii = c(index.radii, np.float64).ctypes.data
+        ix.max_biases = c(index.max_biases, np.float64).ctypes.data
+        ix.log_sizes = c(np.log(np.asarray(index.sizes)), np.float64).ctypes.data  # certify.py:119
+        if self.mode == "spherical":
+            ix.centroid_norms = c(index.centroid_norms, np.float64).ctypes.data
+            ix.angulars = c(index.angulars, np.float64).ctypes.data
+            ix.max_norms = c(index.max_norms, np.float64).ctypes.data
+            ix.min_norms = c(index.min_norms, np.float64).ctypes.data
+        self._ctx = ctypes.c_void_p()
+        rc = lib.csvd_create(ctypes.byref(self._ctx), device, ctypes.byref(td), ctypes.byref(ix))
+        if rc != 0:
+            msg = lib.csvd_strerror(self._ctx).decode()
+            lib.csvd_destroy(self._ctx)
+            self._ctx = None
+            _raise(rc, msg)
+        self._lib = lib
+        self._lock = threading.Lock()
+        self._res = _lib.Result()
+        self._ids = np.empty(self.V, dtype=np.int64)
+        self._logits = np.empty(self.V, dtype=np.float64)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.csvd_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(),
+                ctypes.c_int32(), ctypes.c_int32()]
+        self._check(self._lib.csvd_info(self._ctx, *[ctypes.byref(v) for v in vals]))
+        keys = ("V", "d", "C", "bounds_dim", "w_plan_regular", "b_plan_regular", "grid_ctas")
+        return {k: v.value for k, v in zip(keys, vals)}
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(rc, self._lib.csvd_strerror(self._ctx).decode())
+
+    # --- config -----------------------------------------------------------
+    def make_config(self, cfg, k_max=None, variant=_lib.VARIANT_INCREMENTAL,
+                    first_wave_tokens: int = 0) -> _lib.Config:
+        return config_struct(cfg, self.V, k_max, variant, first_wave_tokens)
+
+    # --- step -------------------------------------------------------------
+    def step(self, h, cfg, k_max=None, variant=_lib.VARIANT_INCREMENTAL) -> DecodeOutcome:
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        if h.shape != (self.d,):
+            raise ValueError(f"query must have length {self.d}")
+        c = cfg if isinstance(cfg, _lib.Config) else self.make_config(cfg, k_max, variant)
+        with self._lock:
+            rc = self._lib.csvd_step_host(self._ctx, h.ctypes.data, ctypes.byref(c), ctypes.byref(self._res),
+                                          self._ids.ctypes.data, self._logits.ctypes.data, self.V)
+            self._check(rc)
+            r = self._res
+            n = int(r.sub_size)
+            ids = self._ids[:n].copy()
+            logits = self._logits[:n].copy()
+        return self._outcome(r, ids, logits)
+
+    def _outcome(self, r, ids, logits) -> DecodeOutcome:
+        kind = _lib.KIND_NAMES.get(r.kind)
+        if kind is None:
+            raise CsvdError(f"device returned no certificate (kind={r.kind})")
+        fb = _lib.FB_NAMES[r.fallback]
+        status = CertStatus(kind, float(r.epsilon_achieved), float(r.u_max), float(r.topk_min))
+        n = int(r.sub_size)
+        stats = StepMetrics(
+            sub_size=n,
+            ratio=n / self.V,
+            clusters_opened=int(r.clusters_opened),
+            xi=float(r.xi),
+            cert_kind=kind,
+            fallback=fb,
+            rho=float(r.rho),
+            flops_sparse=2 * n * self.d,
+            flops_bounds=2 * self.C * self.bounds_dim,
+            heap_pops=int(r.heap_pops),
+        )
+        return DecodeOutcome(token_ids=ids, logits=logits, status=status, fallback_used=fb, stats=stats)
+
+    def bounds(self, h, slack_mode="none"):
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        vals = np.empty(self.C, dtype=np.float64)
+        qn = ctypes.c_double()
+        sl = ctypes.c_double()
+        with self._lock:
+            self._check(self._lib.csvd_bounds_host(self._ctx, h.ctypes.data, 1 if slack_mode == "f32" else 0,
+                                                   vals.ctypes.data, ctypes.byref(qn), ctypes.byref(sl)))
+        return vals, qn.value, sl.value
+
+    def dense(self, h) -> np.ndarray:
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        if h.shape != (self.d,):
+            raise ValueError(f"query must have shape ({self.d},), got {h.shape}")
+        out = np.empty(self.V, dtype=np.float64)
+        with self._lock:
+            self._check(self._lib.csvd_dense_host(self._ctx, h.ctypes.data, out.ctypes.data))
+        return out
+
+
+def config_struct(cfg, V: int, k_max=None, variant=_lib.VARIANT_INCREMENTAL,
+                  first_wave_tokens: int = 0) -> _lib.Config:
+    """DecodeConfig (reference or mirror) -> csvd_config (include/csvd_b200.h)."""
+    validate_config(cfg, V)  # decode.py:325 cfg.validate(V) -> ConfigError
+    km = resolved_k_max(cfg, V) if k_max is None else int(k_max)
+    c = _lib.Config()
+    c.k = int(cfg.k)
+    c.n_targets = len(cfg.targets)
+    for i, t in enumerate(cfg.targets):
+        c.targets[i] = _lib.TARGET_CODES[t]
+    levels = list(cfg.fallback)
+    names = []
+    for lv in levels:
+        name = getattr(lv, "name", None)
+        if name not in _lib.FB_CODES:
+            raise ConfigError(f"unknown fallback level {lv!r}")
+        names.append(name)
+    if "full_vocab" not in names:  # decode.py:303-304
+        levels.append(None)
+        names.append("full_vocab")
+    if len(levels) > _lib.CSVD_MAX_LEVELS:
+        raise ConfigError(f"at most {_lib.CSVD_MAX_LEVELS} fallback levels supported")
+    c.n_levels = len(levels)
+    for i, (lv, name) in enumerate(zip(levels, names)):
+        c.level_kind[i] = _lib.FB_CODES[name]
+        if name == "partial_expand":
+            c.level_param[i] = float(int(lv.delta_c))
+        elif name == "relax_eps":
+            c.level_param[i] = float(lv.factor)
+    c.epsilon = float(cfg.epsilon)
+    c.k_max = max(0, min(int(km), V))
+    c.variant = variant
+    sm = getattr(cfg, "slack_mode", "none")
+    if sm not in ("none", "f32"):
+        raise ValueError(f"unknown slack mode {sm!r}")
+    c.slack_f32 = 1 if sm == "f32" else 0
+    c.first_wave_tokens = int(first_wave_tokens)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# context cache: one upload per (table, index) pair
+# ---------------------------------------------------------------------------
+_CACHE: dict = {}
+_CACHE_LOCK = threading.Lock()
+DEFAULT_DEVICE = 0
+
+
+def _cache_get(key, objs, factory):
+    with _CACHE_LOCK:
+        ent = _CACHE.get(key)
+        if ent is not None:
+            refs, ctx = ent
+            if all(r() is o for r, o in zip(refs, objs)):
+                return ctx
+        ctx = factory()
+        refs = tuple(weakref.ref(o) for o in objs)
+        _CACHE[key] = (refs, ctx)
+        return ctx
+
+
+def prepare(table, index, device: int | None = None) -> DeviceIndex:
+    """Upload (table, index) once; later steps on the same objects reuse it."""
+    dev = DEFAULT_DEVICE if device is None else device
+    return _cache_get(("ti", id(table), id(index), dev), (table, index),
+                      lambda: DeviceIndex(table, index, dev))
+
+
+def clear_cache():
+    with _CACHE_LOCK:
+        for _, ctx in _CACHE.values():
+            ctx.close()
+        _CACHE.clear()
+
+
+def decode_step(table, index, h, cfg, k_max=None) -> DecodeOutcome:
+    """B200 `csvd.decode_step` (decode.py:312-343)."""
+    ctx = prepare(table, index)
+    return ctx.step(h, ctx.make_config(cfg, k_max, _lib.VARIANT_INCREMENTAL))
+
+
+def decode_step_batchselect(table, index, h, cfg, k_max=None) -> DecodeOutcome:
+    """B200 `csvd.decode_step_batchselect` (decode.py:362-382)."""
+    ctx = prepare(table, index)
+    return ctx.step(h, ctx.make_config(cfg, k_max, _lib.VARIANT_BATCHSELECT))
+
+
+class _TrivialIndex:
+    """Single cluster covering the table in original order (dense-only context)."""
+
+    def __init__(self, table):
+        V, d = table.vocab_size, table.hidden_dim
+        self.mode = "euclidean"
+        self.vocab_size = V
+        self.hidden_dim = d
+        self.n_clusters = 1
+        self.perm = np.arange(V, dtype=np.int64)
+        self.starts = np.zeros(1, dtype=np.int64)
+        self.sizes = np.array([V], dtype=np.int64)
+        self.centroids = np.zeros((1, d))
+        self.radii = np.zeros(1)
+        self.max_biases = np.zeros(1)
+        self.fingerprint = None
+
+
+def _bounds_ctx(index, device=None) -> DeviceIndex:
+    dev = DEFAULT_DEVICE if device is None else device
+    return _cache_get(("i", id(index), dev), (index,),
+                      lambda: DeviceIndex(None, index, dev, check_fingerprint=False))
+
+
+def cluster_bounds(index, h, query_norm=None, slack_mode: str = "none") -> BoundVector:
+    """B200 `csvd.cluster_bounds` (bounds.py:178-184).
+
+    query_norm: the reference lets callers pass a precomputed norm; the
+    device always computes ||h|| itself with the reference's arithmetic, so a
+    caller-supplied value must equal it (it does for l2_norm(h))."""
+    if slack_mode not in ("none", "f32"):
+        raise ValueError(f"unknown slack mode {slack_mode!r}")
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    d = index.hidden_dim
+    if index.mode == "bias_augmented" and h.shape == (d + 1,):
+        if h[d] != 1.0:
+            raise ValueError("augmented query must end in 1.0")
+        h = h[:d]
+    if h.shape != (d,):
+        raise ValueError(f"query must have length {d}")
+    ctx = _bounds_ctx(index)
+    vals, qn, sl = ctx.bounds(h, slack_mode)
+    if query_norm is not None and float(query_norm) != qn:
+        raise ValueError("query_norm override differs from the device-computed ||h||")
+    return BoundVector(values=vals, mode=index.mode, query_norm=qn, slack=sl)
+
+
+def dense_logits(table, h) -> DenseResult:
+    """B200 `oracle.dense_logits` (oracle.py:33-41).
+
+    logits: the hand-written full-vocabulary GEMV (same kernel as the
+    full_vocab fallback), bit-equal to the reference; probs / order are
+    derived on the host exactly as the reference does (numpy exp, lexsort)."""
+    h = np.asarray(h, dtype=np.float64)
+    if h.shape != (table.hidden_dim,):
+        raise ValueError(f"query must have shape ({table.hidden_dim},), got {h.shape}")
+    ctx = _cache_get(("t", id(table), DEFAULT_DEVICE), (table,),
+                     lambda: DeviceIndex(table, _TrivialIndex(table), DEFAULT_DEVICE, check_fingerprint=False))
+    logits = ctx.dense(h)
+    m = float(logits.max())
+    lse = m + float(np.log(np.exp(logits - m).sum()))
+    probs = np.exp(logits - lse)
+    order = np.lexsort((np.arange(logits.size), -logits))
+    return DenseResult(logits=logits, probs=probs, order=order)

@@ -1,0 +1,115 @@
+"""GPU parity: the CUDA path through the C ABI vs the reference's own outputs
+(golden fixtures) and vs the oracle at larger sizes.
+
+Bar (BASELINE north star + SURVEY §8c): token ids (as a sequence), logits
+(f64 bit patterns), certificate kind, fallback level, clusters opened,
+heap pops, u_max, k-th logit, xi and the bound vector are bit-exact;
+rho / epsilon_achieved within 1e-12 relative (transcendentals, ~1 ulp).
+"""
+
+import numpy as np
+import pytest
+
+import csvd_oracle as O
+from conftest import TRANS_RTOL, GoldenCase, assert_outcome, golden_names, has_gpu
+import paper_2511_21702_b200 as P
+from paper_2511_21702_b200 import workload as wl
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a GPU")]
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_decode_matches_reference_goldens(name):
+    case = GoldenCase(name)
+    T, ix = case.table, case.index
+    for st in case.steps():
+        fn = P.decode_step if st["variant"] == "incremental" else P.decode_step_batchselect
+        out = fn(T, ix, st["h"], st["cfg"], k_max=st["k_max"])
+        assert_outcome(out, case.expected(st["i"]), rtol=TRANS_RTOL, where=f"{name}[{st['i']}]")
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_bounds_match_reference_goldens(name):
+    case = GoldenCase(name)
+    ix = case.index
+    seen = set()
+    for st in case.steps():
+        key = (int(np.flatnonzero((case.z["queries"] == st["h"]).all(axis=1))[0]), st["cfg"].slack_mode)
+        if key in seen:
+            continue
+        seen.add(key)
+        exp = case.expected(st["i"])
+        b = P.cluster_bounds(ix, st["h"], slack_mode=st["cfg"].slack_mode)
+        if ix.mode == "spherical":  # acos/cos: ulp-level libm differences
+            np.testing.assert_allclose(b.values, exp["U"], rtol=1e-12, atol=0)
+        else:
+            assert np.array_equal(b.values, exp["U"]), f"{name}: bounds not bit-equal"
+        assert b.query_norm == exp["qn"]
+        assert b.slack == exp["slack"]
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_dense_matches_reference_goldens(name):
+    case = GoldenCase(name)
+    for i, ref in enumerate(case.z["dense"]):
+        r = P.dense_logits(case.table, case.z["queries"][i])
+        assert np.array_equal(r.logits, ref)
+
+
+def _c1_like(V=32000, d=4096, n_modes=128, g=2, dtype="f32"):
+    T = wl.synth_vocab(V, d, n_modes, 0.3, 1, dtype=dtype)
+    ix = wl.fast_index(T, n_modes, g)
+    return T, ix
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_c1_shape_vs_oracle(dtype):
+    """c1 shape (V=32000, d=4096, C=256): GPU vs oracle, mixed workloads."""
+    T, ix = _c1_like(dtype=dtype)
+    q = np.vstack([wl.generate_queries(6, 4096, "contextual", 7, centroids=ix.centroids),
+                   wl.generate_queries(2, 4096, "random", 8)])
+    cfgs = [P.DecodeConfig(k=10), P.DecodeConfig(k=10, epsilon=1e-3, targets=("softmax_eps",)),
+            P.DecodeConfig(k=10, k_max=600)]
+    for ci, cfg in enumerate(cfgs):
+        for i, h in enumerate(q):
+            exp = O.decode_step(T, ix, h, cfg)
+            got = P.decode_step(T, ix, h, cfg)
+            e = _fields(exp)
+            assert_outcome(got, e, rtol=TRANS_RTOL, where=f"c1[{dtype},{ci},{i}]")
+
+
+def _fields(o):
+    st = o.stats
+    return dict(ids=o.token_ids, logits=o.logits, kind=o.status.kind, fallback=o.fallback_used,
+                sub_size=st["sub_size"], clusters_opened=st["clusters_opened"], heap_pops=st["heap_pops"],
+                flops_sparse=st["flops_sparse"], flops_bounds=st["flops_bounds"], eps=o.status.epsilon_achieved,
+                u_max=o.status.u_max, topk_min=o.status.topk_min, rho=st["rho"], xi=st["xi"], ratio=st["ratio"])
+
+
+def test_many_clusters_64_merge_recompute():
+    """g=80 clusters per mode: certification needs > 64 opens, crossing the
+    full log_z recompute every 64th merge (certify.py:79-83)."""
+    T = wl.synth_vocab(20000, 512, 4, 0.05, 1)
+    ix = wl.fast_index(T, 4, 80)
+    q = wl.generate_queries(4, 512, "contextual", 7, centroids=ix.centroids)
+    for cfg in (P.DecodeConfig(k=10), P.DecodeConfig(k=5, epsilon=1e-2, targets=("softmax_eps",))):
+        for i, h in enumerate(q):
+            exp = O.decode_step(T, ix, h, cfg)
+            got = P.decode_step(T, ix, h, cfg)
+            assert exp.stats["clusters_opened"] >= 1
+            assert_outcome(got, _fields(exp), rtol=1e-11, where=f"g80[{i}]")
+
+
+def test_errors_mirror_reference():
+    T, ix = _c1_like(V=2000, d=512, n_modes=20, g=1)
+    h = wl.generate_queries(1, 512, "random", 1)[0]
+    with pytest.raises(P.ConfigError):
+        P.decode_step(T, ix, h, P.DecodeConfig(k=0))
+    with pytest.raises(P.ConfigError):
+        P.decode_step(T, ix, h, P.DecodeConfig(epsilon=1.5))
+    with pytest.raises(ValueError):
+        P.decode_step(T, ix, h[:10], P.DecodeConfig())
+    bad = wl.index_from_assignment(T, np.arange(2000) % 20)
+    bad.fingerprint = b"x" * 32
+    with pytest.raises(P.ConfigError):
+        P.decode_step(T, bad, h, P.DecodeConfig())
