@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark: CSV-Decode output-layer steps/sec at the Llama-3 8B head shape.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "c2"): V=128256, d=4096, C=1024 clusters,
+batch 1, exact top-k (k=10) + epsilon-softmax targets with the reference's
+default fallback chain, one CUDA-graph replay per step.  Synthetic data:
+`synth_vocab(V, d, n_modes=C/g, spread, seed=1)` with the fast index
+(g clusters per mode) and the reference's contextual query model
+(`generate_queries(..., "contextual", seed=7, noise=0.3)`).
+
+Reported (one JSON line on rank 0):
+  value   device-timed steps/s, inputs resident in HBM, CUDA events on the
+          step's stream around each graph replay, L2 flushed (384 MiB streaming
+          read) between timed steps, so centroids and W rows come from HBM
+  e2e     the same metric through the public API `decode_step(table, index,
+          h, cfg)` with host h in and host token ids / logits out (H2D + D2H
+          inside the timed region)
+  roofline  algorithmic bytes per step / mean step time vs the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the oracle port (oracle/, numpy + threaded C pairwise GEMV)
+          on a bounded sample of the same query stream, this host's cores
+`--impl reference` times only that CPU restatement (the reference is pure
+Python; there is nothing to install or compile) and prints its line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output-layer decode steps/sec at V=128256,d=4096; HBM roofline %; fallback rate"
+UNIT = "steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--V", type=int, default=128256)
+    ap.add_argument("--d", type=int, default=4096)
+    ap.add_argument("--C", type=int, default=1024)
+    ap.add_argument("--g", type=int, default=16, help="clusters per synth mode (|S|/V ~ g/C)")
+    ap.add_argument("--spread", type=float, default=0.3)
+    ap.add_argument("--noise", type=float, default=0.3)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--first-wave-tokens", type=int, default=0)
+    ap.add_argument("--direct", action="store_true", help="launch kernels without the CUDA graph (profiling)")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return f"llama3-8b-head V={a.V} d={a.d} C={a.C} g={a.g} {a.dtype} B=1"
+
+
+def make_workload(a):
+    from paper_2511_21702_b200 import workload as wl
+    n_modes = max(1, a.C // a.g)
+    T = wl.synth_vocab(a.V, a.d, n_modes, a.spread, 1, dtype=a.dtype)
+    ix = wl.fast_index(T, n_modes, a.g)
+    q = wl.generate_queries(a.steps + a.warmup, a.d, "contextual", 7, centroids=ix.centroids, noise=a.noise)
+    return T, ix, q
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def step_bytes(ix, outcome, s_w):
+    """Algorithmic bytes of one step."""
+    C, d = ix.n_clusters, ix.hidden_dim
+    bd = d + (1 if ix.mode == "bias_augmented" else 0)
+    V = ix.vocab_size
+    b = 8 * C * bd + 24 * C + 8 * d
+    if outcome.fallback_used == "full_vocab":
+        return b + V * (s_w * d + 4) + 16 * V
+    n = outcome.stats.sub_size
+    return b + n * (s_w * d + 4) + 12 * n
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx = [], None
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(T, ix, q, cfg, seconds):
+    """The oracle port (oracle/csvd_oracle.py) on a bounded sample of the stream."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import csvd_oracle as O
+    O.set_threads(0)
+    cores = os.cpu_count() or 1
+    O.decode_step(T, ix, q[0], cfg)  # warm (builds nothing, touches pages)
+    n, t0 = 0, time.perf_counter()
+    fb = 0
+    while n < len(q) and (time.perf_counter() - t0) < seconds:
+        out = O.decode_step(T, ix, q[n], cfg)
+        fb += out.fallback_used is not None
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} consecutive steps of the same contextual query stream ({dt:.1f} s), "
+                      f"oracle/csvd_oracle.py decode_step with the per-step SHA-256 fingerprint of the "
+                      f"reference memoized and the pairwise f64 GEMV in C on {cores} threads",
+            "fallback_rate": fb / max(n, 1)}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2511_21702_b200 as P
+    T, ix, q = make_workload(a)
+    cfg = P.DecodeConfig(k=a.k)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import csvd_oracle as O
+    O.set_threads(0)
+    cores = os.cpu_count() or 1
+    for i in range(a.warmup):
+        O.decode_step(T, ix, q[i], cfg)
+    times = []
+    fb = 0
+    budget = a.cpu_seconds * 8
+    t_all = time.perf_counter()
+    n = 0
+    for i in range(a.steps):
+        t0 = time.perf_counter()
+        out = O.decode_step(T, ix, q[a.warmup + i], cfg)
+        times.append(time.perf_counter() - t0)
+        fb += out.fallback_used is not None
+        n += 1
+        if time.perf_counter() - t_all > budget:
+            break
+    tot = sum(times)
+    v = n / tot
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": n, "warmup": a.warmup,
+        "ms_per_step": 1e3 * tot / n, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference synth_vocab + fast index + contextual queries)",
+        "config": {"workload": workload_name(a), "global_batch": 1, "k": a.k, "l2": "n/a (CPU)"},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n} steps of the contextual stream, oracle port of csvd.decode_step "
+                                   f"(fingerprint memoized; pairwise GEMV in C, {cores} threads)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "fallback_rate": fb / n,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import torch
+    import paper_2511_21702_b200 as P
+    from paper_2511_21702_b200 import _lib, engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    engine.DEFAULT_DEVICE = local
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    T, ix, q = make_workload(a)
+    cfg = P.DecodeConfig(k=a.k)
+    ctx = P.prepare(T, ix)
+    lib = _lib.load()
+    import ctypes
+    sp = ctypes.c_void_p()
+    lib.csvd_stream(ctx._ctx, ctypes.byref(sp))
+    ext = torch.cuda.ExternalStream(sp.value, device=local)
+    ccfg = ctx.make_config(cfg, first_wave_tokens=a.first_wave_tokens)
+    if a.direct:
+        lib.csvd_set_direct(ctx._ctx, 1)
+    s_w = 2 if a.dtype == "bf16" else 4
+    K, W = a.steps, a.warmup
+
+    def do_flush():
+        if not a.no_flush:
+            lib.csvd_l2_flush(ctx._ctx, sp)
+
+    # ---- e2e through the public API (host h in, host outcome out) ----------
+    for i in range(W):
+        ctx.step(q[i], ccfg)
+    outs, e2e_t, waves = [], [], []
+    for i in range(K):
+        do_flush()
+        torch.cuda.synchronize(local)
+        t0 = time.perf_counter()
+        o = P.decode_step(T, ix, q[W + i], cfg) if a.first_wave_tokens == 0 else ctx.step(q[W + i], ccfg)
+        e2e_t.append(time.perf_counter() - t0)
+        outs.append(o)
+        waves.append(ctx._res.waves)
+
+    # ---- device-resident timing (value): CUDA events on the step stream ----
+    hq = torch.from_numpy(np.ascontiguousarray(q)).to(local)
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    for i in range(W):
+        lib.csvd_step_device(ctx._ctx, hq[i].data_ptr(), ctypes.byref(ccfg), sp)
+    torch.cuda.synchronize(local)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            do_flush()
+            ev_s[i].record(ext)
+            rc = lib.csvd_step_device(ctx._ctx, hq[W + i].data_ptr(), ctypes.byref(ccfg), sp)
+            ev_e[i].record(ext)
+            if rc != 0:
+                raise RuntimeError(lib.csvd_strerror(ctx._ctx).decode())
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=local, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---- dense full-vocabulary GEMV (K5) on the same stream, for context ----
+    dense_ms = []
+    for i in range(min(K + W, 23)):
+        do_flush()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(ext)
+        lib.csvd_dense_device(ctx._ctx, hq[i].data_ptr(), sp)
+        s1.record(ext)
+        torch.cuda.synchronize(local)
+        if i >= 3:
+            dense_ms.append(s0.elapsed_time(s1))
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk, pk_kind = peaks()
+    bytes_steps = [step_bytes(ix, o, s_w) for o in outs]
+    mean_bytes = float(np.mean(bytes_steps))
+    mean_ms = total_ms / K
+    achieved = mean_bytes / (mean_ms * 1e-3) / 1e9
+    V, d = a.V, a.d
+    dense_bytes = V * (s_w * d + 4) + 8 * d + 16 * V
+    dense_mean = float(np.mean(dense_ms))
+    fallbacks = sum(o.fallback_used is not None for o in outs)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(workload_name(a))
+        except Exception:
+            traffic = None
+    h2d = 8 * d + 152
+    d2h = float(np.mean([88 + 16 * o.stats.sub_size for o in outs]))
+    e2e_v = K / sum(e2e_t)
+    line = {
+        "metric": METRIC,
+        "value": world * K / (total_ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": mean_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: reference synth_vocab mixture (seed 1) + fast index + contextual queries (seed 7)",
+        "config": {"workload": workload_name(a), "global_batch": world, "k": a.k,
+                   "targets": ["topk", "softmax_eps"], "epsilon": 0.05,
+                   "fallback": ["partial_expand:4", "relax_eps:2.0", "full_vocab"],
+                   "weights": a.dtype, "cuda_graph": True,
+                   "l2": "flushed between timed steps (384 MiB streaming read)" if not a.no_flush else "not flushed",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "e2e": {"value": world * e2e_v if world > 1 else e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
+                     "traffic": traffic, "peak_kind": pk_kind,
+                     "kernel": "whole step (k_bounds + k_wave graph)",
+                     "algorithmic_bytes_per_step": mean_bytes},
+        "fallback_rate": fallbacks / K,
+        "mean_sub_ratio": float(np.mean([o.stats.ratio for o in outs])),
+        "mean_clusters_opened": float(np.mean([o.stats.clusters_opened for o in outs])),
+        "p50_ms": float(np.percentile(step_ms, 50)), "p95_ms": float(np.percentile(step_ms, 95)),
+        "dense_gemv": {"ms": dense_mean, "steps_per_s": 1e3 / dense_mean,
+                       "achieved_gbs": dense_bytes / (dense_mean * 1e-3) / 1e9,
+                       "frac": dense_bytes / (dense_mean * 1e-3) / 1e9 / pk},
+        "speedup_vs_dense_gemv": dense_mean / mean_ms,
+        "gpu_launches": int(sum(1 + w for w in waves)),
+        "clocks": clk.summary(),
+    }
+    if not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(T, ix, q[W:], cfg, a.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

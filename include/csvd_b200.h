@@ -144,8 +144,8 @@ int csvd_reserve_k(csvd_ctx *ctx, int32_t k);
 int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config *cfg,
                    csvd_result *res, int64_t *ids, double *logits, int64_t cap);
 
-/* Device-resident variant: h_dev is a device pointer to bd doubles (or d for
- * bias_augmented: the engine appends the 1.0), nothing is copied back; read
+/* Device-resident variant: h_dev is a device pointer to d doubles (the
+ * bias-augmented [h, 1] is formed on the device), nothing is copied back; read
  * results with csvd_outputs().  Asynchronous on `stream`. */
 int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_config *cfg,
                      void *stream);
@@ -167,6 +167,19 @@ int csvd_dense_device(csvd_ctx *ctx, const double *h_dev, void *stream);
 /* Introspection for tests / bench. */
 int csvd_info(csvd_ctx *ctx, int64_t *V, int64_t *d, int32_t *C, int32_t *bd,
               int32_t *w_plan_regular, int32_t *b_plan_regular, int32_t *grid_ctas);
+
+/* The context's own CUDA stream (cudaStream_t as void*): callers that time
+ * or order work around csvd_*_device calls record events on it. */
+int csvd_stream(csvd_ctx *ctx, void **stream);
+
+/* Launch the step's kernels directly instead of replaying the CUDA graph
+ * (identical results; for per-kernel profiling, since profilers cannot see
+ * into conditional graph nodes).  The host then syncs once per wave. */
+int csvd_set_direct(csvd_ctx *ctx, int32_t direct);
+
+/* Benchmark utility: stream-read a 384 MiB buffer on `stream` so the next step
+ * starts with an L2 holding none of its inputs (and no dirty lines). */
+int csvd_l2_flush(csvd_ctx *ctx, void *stream);
 
 /* Kernel launch counter (number of kernels launched by the last step call,
  * counting graph kernel nodes executed; diagnostic for bench gpu_launches). */

@@ -94,7 +94,8 @@ class Result(ctypes.Structure):
 EXPORTS = (
     "csvd_create", "csvd_destroy", "csvd_strerror", "csvd_reserve_k", "csvd_step_host",
     "csvd_step_device", "csvd_outputs", "csvd_bounds_host", "csvd_dense_host",
-    "csvd_dense_device", "csvd_info", "csvd_last_launches",
+    "csvd_dense_device", "csvd_info", "csvd_last_launches", "csvd_stream", "csvd_set_direct",
+    "csvd_l2_flush",
 )
 
 _lib = None
@@ -134,8 +135,12 @@ def load():
     lib.csvd_dense_device.argtypes = [P, P, P]
     lib.csvd_info.argtypes = [P, P, P, P, P, P, P, P]
     lib.csvd_last_launches.argtypes = [P, P]
+    lib.csvd_stream.argtypes = [P, vp]
+    lib.csvd_set_direct.argtypes = [P, ctypes.c_int32]
+    lib.csvd_l2_flush.argtypes = [P, P]
+    lib.csvd_test_sizes.argtypes = [P, P, P, P]
     lib.csvd_test_scan_host.argtypes = [
-        ctypes.POINTER(Config), ctypes.c_int, ctypes.c_longlong, ctypes.c_int, P, P, P, P, P, P, P, P,
+        ctypes.POINTER(Config), ctypes.c_int, ctypes.c_longlong, ctypes.c_int, P, P, P, P, P, P, P,
         ctypes.c_int, P, ctypes.c_int, ctypes.POINTER(Result), P, P]
     for name in EXPORTS:
         getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int

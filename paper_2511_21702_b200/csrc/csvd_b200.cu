@@ -55,7 +55,8 @@ struct Dev {
     // per step
     const double *h;          // [d]
     const csvd_config *cfg;
-    double *U, *X, *dots;     // [C]
+    double *U, *X, *dots;     // [C] by cluster id
+    double *Uo;               // [C] bounds in opening order
     int *order;               // [C]
     int *cum;                 // [C+1]
     double *lrh;              // [C+1]
@@ -70,6 +71,8 @@ struct Dev {
     csvd_result *res;
     unsigned int *counters;   // [0] bounds CTAs, [1] wave clusters, [2] dense CTAs
     cudaGraphConditionalHandle loop;
+    int scan_smem_doubles;    // dynamic smem of k_wave, in doubles
+    unsigned long long *dbg;  // optional phase timestamps
     int use_graph;            // 1 -> set the conditional handle
     int bounds_only;          // 1 -> skip ordering/planning
     int dense_only;           // 1 -> (dense API) start directly in dense mode
@@ -78,6 +81,16 @@ struct Dev {
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
+// debug phase timestamps (%globaltimer, ns), enabled by CSVD_DEBUG_TS=1
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DBG_TS(D, slot)                                              \
+    do {                                                             \
+        if ((D).dbg) (D).dbg[(slot)] = gtimer();                     \
+    } while (0)
 __device__ __forceinline__ unsigned long long dkey(double v) {
     unsigned long long u = (unsigned long long)__double_as_longlong(v);
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
@@ -118,16 +131,41 @@ __device__ __forceinline__ double set_cond(const Dev &D, unsigned v) {
 // ---------------------------------------------------------------------------
 // warp-level primitives for the scan
 // ---------------------------------------------------------------------------
+struct WarpSearch {
+    // first i in [lo, hi) with pred(i) true (pred monotone), or hi.
+    // 32 probes per round, so ~2 dependent rounds for C <= 1024.
+    template <class F>
+    __device__ int operator()(int lo, int hi, const F &pred) const {
+        const int lane = threadIdx.x & 31;
+        while (hi - lo > 32) {
+            const int step = (hi - lo + 31) / 32;
+            const int probe = lo + lane * step;
+            const bool t = probe < hi ? pred(probe) : true;
+            const unsigned m = __ballot_sync(CSVD_FULL, t);
+            if (m == 0) {
+                lo = lo + 31 * step + 1;
+            } else {
+                const int f = __ffs(m) - 1;
+                const int pf = lo + f * step;
+                const int nlo = f == 0 ? lo : lo + (f - 1) * step + 1;
+                hi = pf < hi ? pf : hi;
+                lo = nlo;
+            }
+        }
+        const int probe = lo + lane;
+        const bool t = probe < hi ? pred(probe) : true;
+        const unsigned m = __ballot_sync(CSVD_FULL, t);
+        return m == 0 ? hi : lo + (__ffs(m) - 1);
+    }
+};
+
 struct WarpPrims {
     int lane;
-    double *bbuf;  // shared scratch for the incoming list
+    double *bbuf;  // unused (lists are prefetched into shared memory)
     // top-k of union of two descending lists (values only), warp-parallel
     // merge-path: element i of A lands at i + #{B > A[i]}, element j of B at
     // j + #{A >= B[j]}.
-    __device__ int merge_topk(const double *A, int ka, const double *Bg, int kb, int k, double *out) {
-        for (int j = lane; j < kb; j += 32) bbuf[j] = __ldcg(Bg + j);
-        __syncwarp();
-        const double *B = bbuf;
+    __device__ int merge_topk(const double *A, int ka, const double *B, int kb, int k, double *out) {
         for (int i = lane; i < ka; i += 32) {
             double a = A[i];
             int lo = 0, hi = kb;  // count B > a
@@ -322,8 +360,10 @@ __global__ void __launch_bounds__(THREADS) k_bounds(Dev D) {
     double *scratch = smem + D.bd + warp * CSVD_MAX_LEAVES / 4;  // generic leaf sums
     __shared__ double s_qn;
     __shared__ int s_last;
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 0);
     pw_stage_h(D.bplan, D.h, D.d, hs);
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 1);
     if (warp == 0) {
         double ss;
         if constexpr (CPL > 0) {
@@ -338,6 +378,7 @@ __global__ void __launch_bounds__(THREADS) k_bounds(Dev D) {
         if (lane == 0) s_qn = __dsqrt_rn(ss);
     }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 2);
     const double qn = s_qn;
     for (int c = blockIdx.x * WARPS + warp; c < D.C; c += gridDim.x * WARPS) {
         double dot = warp_dot_t<double, CPL, Q>(D.cent + (size_t)c * D.bd, hs, D.bplan, scratch, lane);
@@ -360,10 +401,15 @@ __global__ void __launch_bounds__(THREADS) k_bounds(Dev D) {
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 3);
     if (!s_last) return;
     __threadfence();
-    if (threadIdx.x == 0) D.counters[0] = 0;
+    if (threadIdx.x == 0) {
+        D.counters[0] = 0;
+        DBG_TS(D, 4);
+    }
     last_cta_order(D, smem, qn);
+    if (threadIdx.x == 0) DBG_TS(D, 9);
 }
 
 // Suffix log-sum-exp combine: (m, s) represents m + log(s)
@@ -378,10 +424,18 @@ __device__ __forceinline__ void lse_combine(double &m, double &s, double m2, dou
     }
 }
 
+// Shared-memory layout of the last CTA (all sizes padded to cpad):
+//   keyU[cpad] f64  sorted bounds (= Uo)      keyI[cpad] i32  order
+//   cumS[cpad+1] i32 prefix token counts      lrhS[cpad+1] f64 suffix LSE
 __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double qn) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const csvd_config &cfg = *D.cfg;
     const int C = D.C;
+    const int n = D.cpad;
+    double *keyU = smem;
+    double *lrhS = smem + n;
+    int *keyI = reinterpret_cast<int *>(smem + 2 * n + 1);
+    int *cumS = keyI + n;
     __shared__ double s_red[THREADS];
     __shared__ int s_flag;
     // --- slack (bounds.py:58-64) + finiteness (bounds.py:53-55)
@@ -402,21 +456,8 @@ __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double q
     }
     double eta = 0.0;
     if (cfg.slack_f32) eta = __dmul_rn(__dmul_rn(4.0, 1.1920928955078125e-07), s_red[0]);
-    __syncthreads();
-    if (s_flag) {
-        if (tid == 0) {
-            D.res->error = CSVD_EVALUE;
-            D.res->query_norm = qn;
-            D.st->phase = PH_ERROR;
-            D.st->mode = MODE_IDLE;
-            set_cond(D, 0);
-        }
-        return;
-    }
     // --- final U, X = log|c| + U (certify.py:119 order), sort keys
-    double *keyU = smem;                                   // [cpad]
-    int *keyI = reinterpret_cast<int *>(smem + D.cpad);    // [cpad]
-    for (int c = tid; c < D.cpad; c += nt) {
+    for (int c = tid; c < n; c += nt) {
         if (c < C) {
             double u = __dadd_rn(__ldcg(D.U + c), eta);
             if (!isfinite(u)) atomicOr(&s_flag, 1);
@@ -434,30 +475,25 @@ __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double q
         D.res->query_norm = qn;
         D.res->slack = eta;
     }
-    if (s_flag) {
+    if (s_flag || D.bounds_only) {
         if (tid == 0) {
-            D.res->error = CSVD_EVALUE;
-            D.st->phase = PH_ERROR;
+            if (s_flag) D.res->error = CSVD_EVALUE;
+            D.st->phase = s_flag ? PH_ERROR : PH_DONE;
             D.st->mode = MODE_IDLE;
             set_cond(D, 0);
         }
         return;
     }
-    if (D.bounds_only) {
-        if (tid == 0) { D.st->mode = MODE_IDLE; set_cond(D, 0); }
-        return;
-    }
+    if (tid == 0) DBG_TS(D, 5);
     // --- bitonic sort: descending U, ascending id  (np.lexsort((arange, -U)))
-    const int n = D.cpad;
     for (int size = 2; size <= n; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = tid; t < n / 2; t += nt) {
                 int lo = 2 * t - (t & (stride - 1));
                 int hi = lo + stride;
-                bool desc = ((lo & size) == 0);  // "first comes first" segments
+                bool desc = ((lo & size) == 0);
                 double ua = keyU[lo], ub = keyU[hi];
                 int ia = keyI[lo], ib = keyI[hi];
-                // a before b in final order?  (ua > ub) || (ua == ub && ia < ib)
                 bool a_first = (ua > ub) || (ua == ub && ia < ib);
                 if (a_first != desc) {
                     keyU[lo] = ub; keyU[hi] = ua;
@@ -467,16 +503,13 @@ __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double q
             __syncthreads();
         }
     }
-    // --- order + prefix token counts (block scan, chunked)
+    if (tid == 0) DBG_TS(D, 6);
+    // --- order, Uo, prefix token counts (block scan over contiguous chunks)
     __shared__ int s_scan[THREADS];
     const int per = (C + nt - 1) / nt;
-    const int b0 = tid * per, b1 = min(C, b0 + per);
+    const int b0 = min(C, tid * per), b1 = min(C, b0 + per);
     int local = 0;
-    for (int p = b0; p < b1; ++p) {
-        int c = keyI[p];
-        D.order[p] = c;
-        local += D.sizes[c];
-    }
+    for (int p = b0; p < b1; ++p) local += D.sizes[keyI[p]];
     s_scan[tid] = local;
     __syncthreads();
     for (int o = 1; o < nt; o <<= 1) {
@@ -487,18 +520,17 @@ __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double q
     }
     int run = s_scan[tid] - local;
     for (int p = b0; p < b1; ++p) {
-        D.cum[p] = run;
+        cumS[p] = run;
         run += D.sizes[keyI[p]];
     }
-    if (tid == nt - 1) D.cum[C] = s_scan[nt - 1];
+    if (tid == nt - 1) cumS[C] = s_scan[nt - 1];
     // --- suffix log-sum-exp over x[order[q]], q >= p  -> lrh[p]
     __shared__ double s_m[THREADS], s_s[THREADS];
-    double m = -INFINITY, s = 0.0;
-    for (int p = b1 - 1; p >= b0; --p) lse_combine(m, s, D.X[keyI[p]], 1.0);
+    double m = -INFINITY, sm = 0.0;
+    for (int p = b1 - 1; p >= b0; --p) lse_combine(m, sm, __ldcg(D.X + keyI[p]), 1.0);
     s_m[tid] = m;
-    s_s[tid] = s;
+    s_s[tid] = sm;
     __syncthreads();
-    // inclusive suffix scan over thread aggregates
     for (int o = 1; o < nt; o <<= 1) {
         double m2 = -INFINITY, s2 = 0.0;
         if (tid + o < nt) { m2 = s_m[tid + o]; s2 = s_s[tid + o]; }
@@ -509,65 +541,56 @@ __device__ __noinline__ void last_cta_order(const Dev &D, double *smem, double q
         s_s[tid] = ss;
         __syncthreads();
     }
-    // exclusive suffix for this chunk = aggregate of threads > tid
     m = (tid + 1 < nt) ? s_m[tid + 1] : -INFINITY;
-    s = (tid + 1 < nt) ? s_s[tid + 1] : 0.0;
+    sm = (tid + 1 < nt) ? s_s[tid + 1] : 0.0;
     for (int p = b1 - 1; p >= b0; --p) {
-        lse_combine(m, s, D.X[keyI[p]], 1.0);
-        D.lrh[p] = (m == -INFINITY) ? -INFINITY : __dadd_rn(m, log(s));
+        lse_combine(m, sm, __ldcg(D.X + keyI[p]), 1.0);
+        lrhS[p] = (m == -INFINITY) ? -INFINITY : __dadd_rn(m, log(sm));
     }
-    if (tid == 0) D.lrh[C] = -INFINITY;
-    __threadfence();
+    if (tid == 0) lrhS[C] = -INFINITY;
     __syncthreads();
-    // --- init scan state + plan wave 1 (single thread)
+    if (tid == 0) DBG_TS(D, 7);
+    // --- publish order / Uo / cum / lrh, reset per-cluster counters
+    for (int p = tid; p < C; p += nt) {
+        D.order[p] = keyI[p];
+        D.Uo[p] = keyU[p];
+        D.cum[p] = cumS[p];
+        D.lrh[p] = lrhS[p];
+        D.cl_done[p] = 0;
+    }
     if (tid == 0) {
+        D.cum[C] = cumS[C];
+        D.lrh[C] = lrhS[C];
+    }
+    // --- init scan state + plan wave 1 (thread 0, from shared memory)
+    if (tid == 0) {
+        DBG_TS(D, 8);
         ScanState st;
         memset(&st, 0, sizeof(st));
         st.phase = PH_MAIN;
         st.log_z = -INFINITY;
         st.smin = INFINITY;
         st.smax = -INFINITY;
-        int sum_dc = 0;
-        for (int l = 0; l < cfg.n_levels; ++l)
-            if (cfg.level_kind[l] == CSVD_FB_PARTIAL_EXPAND) sum_dc += (int)cfg.level_param[l];
-        if (cfg.variant == CSVD_VARIANT_BATCHSELECT) {
-            // _select_by_bound (decode.py:346-359)
-            long long total = 0;
-            int sel = 0;
-            for (int p = 0; p < C; ++p) {
-                long long sz = D.sizes[D.order[p]];
-                if (sel > 0 && total + sz > cfg.k_max) break;
-                sel++;
-                total += sz;
-                if (total >= cfg.k_max) break;
-            }
-            st.p_sel = sel;
-            st.p_cap = min(C, sel + sum_dc);
-        } else {
-            int pe = 1, phi = C + 1;  // first prefix with cum > k_max
-            while (pe < phi) {
-                int mid = (pe + phi) / 2;
-                if ((long long)D.cum[mid] > cfg.k_max) phi = mid; else pe = mid + 1;
-            }
-            st.p_cap = min(C, min(pe, C) + sum_dc);
-            st.p_sel = 0;
-        }
+        ScanIn in{D.cfg, C, (long long)D.V, D.d, cumS, keyU, lrhS, nullptr, nullptr, nullptr, nullptr, D.K, nullptr};
+        ScalarSearch search;
+        st.p_sel = (cfg.variant == CSVD_VARIANT_BATCHSELECT) ? csvd_select_prefix(in, cfg.k_max, search) : 0;
+        st.p_cap = csvd_cap_prefix(in, st.p_sel, search);
         long long wt = cfg.first_wave_tokens > 0 ? cfg.first_wave_tokens : 1;
         st.wave_tokens = (int)min(wt, (long long)D.V);
-        const int c0 = D.order[0];
-        st.est = __dadd_rn(D.dots[c0], D.meanb[c0]);
-        if (D.mode == CSVD_MODE_BIAS_AUGMENTED) st.est = D.dots[c0];
-        ScanIn in{D.cfg, C, (long long)D.V, D.d, D.order, D.cum, D.U, D.lrh, nullptr, nullptr, nullptr,
-                  nullptr, D.K, nullptr};
-        int hi = csvd_plan_wave(st, in);
-        start_wave(D, st, hi);
+        const int c0 = keyI[0];
+        st.est = (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? __ldcg(D.dots + c0) : __dadd_rn(__ldcg(D.dots + c0), D.meanb[c0]);
+        int hi = csvd_plan_wave(st, in, search);
+        st.p_lo = 0;
+        st.p_hi = hi;
+        st.row_lo = 0;
+        st.row_hi = cumS[hi];
+        st.mode = MODE_SPARSE;
         st.wave_tokens = st.wave_tokens * 2 < D.V ? st.wave_tokens * 2 : (int)D.V;
         *D.st = st;
         D.counters[1] = 0;
         D.res->error = 0;
         D.res->waves = 0;
     }
-    for (int q = tid; q < C; q += nt) D.cl_done[q] = 0;
     __threadfence();
     __syncthreads();
     if (tid == 0) set_cond(D, 1);
@@ -598,8 +621,10 @@ __global__ void __launch_bounds__(THREADS) k_wave(Dev D) {
     }
     double *hs = smem;
     double *scratch = smem + D.d + warp * (CSVD_MAX_LEAVES / 4);
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 16 + 8 * (st0.iter & 1));
     pw_stage_h(D.wplan, D.h, D.d, hs);
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 17 + 8 * (st0.iter & 1));
     if (st0.mode == MODE_SPARSE)
         wave_sparse<ET, CPL, Q>(D, st0, hs, scratch, smem, lane, gwarp, nwarps);
     else
@@ -607,23 +632,58 @@ __global__ void __launch_bounds__(THREADS) k_wave(Dev D) {
 }
 
 __device__ __noinline__ void run_scan(const Dev &D, const ScanState &st0, double *smem_base, int lane) {
-    // all wave clusters are summarised; this warp owns the sequential scan.
+    // All wave clusters are summarised; this warp owns the sequential scan.
     // Every lane runs the identical scalar state machine (uniform control
     // flow); collective primitives are warp-parallel; lane 0 writes state.
+    // Inputs are prefetched chunk by chunk into shared memory with one round
+    // of parallel loads, so the sequential part never waits on L2.
     ScanState st = st0;
     csvd_result res;
     memset(&res, 0, sizeof(res));
     const int K = D.K;
-    double *ra = smem_base, *rb = smem_base + K, *bbuf = smem_base + 2 * K;
+    const int k = D.cfg->k;
+    if (lane == 0) DBG_TS(D, 19 + 8 * (st0.iter & 1));
+    double *ra = smem_base, *rb = smem_base + K;
+    double *chunk = smem_base + 2 * K;
+    int M = (D.scan_smem_doubles - 2 * K - 8) / (k + 6);
+    if (M > 64) M = 64;
+    if (M < 1) M = 1;
+    double *Uo_s = chunk, *lrh_s = chunk + (M + 1), *lse_s = chunk + 2 * (M + 1);
+    double *min_s = lse_s + M, *max_s = min_s + M, *topk_s = max_s + M;
+    int *cum_s = reinterpret_cast<int *>(topk_s + (size_t)M * k);
     for (int i = lane; i < st.kcount; i += 32) ra[i] = __ldcg(D.run_a + i);
     __syncwarp();
     double *run = ra, *run_alt = rb;
-    WarpPrims prims{lane, bbuf};
-    ScanIn in{D.cfg, D.C, (long long)D.V, D.d, D.order, D.cum, D.U, D.lrh, D.sum_lse, D.sum_min, D.sum_max,
-              D.sum_topk, D.K, D.S_logits};
-    Scan<WarpPrims> sc{in, st, run, run_alt, prims, res};
-    sc.run(st.p_hi);
+    WarpPrims prims{lane, nullptr};
+    int q0 = st.p;
+    while (q0 < st.p_hi && (st.phase == PH_MAIN || st.phase == PH_PE)) {
+        const int q1 = min(st.p_hi, q0 + M);
+        const int nq = q1 - q0;
+        for (int i = lane; i <= nq; i += 32) {
+            const int q = q0 + i;
+            cum_s[i] = __ldcg(D.cum + q);
+            Uo_s[i] = q < D.C ? __ldcg(D.Uo + q) : -INFINITY;
+            lrh_s[i] = __ldcg(D.lrh + q);
+            if (i < nq) {
+                lse_s[i] = __ldcg(D.sum_lse + q);
+                min_s[i] = __ldcg(D.sum_min + q);
+                max_s[i] = __ldcg(D.sum_max + q);
+            }
+        }
+        for (int e = lane; e < nq * k; e += 32) {
+            const int i = e / k, j = e - i * k;
+            topk_s[e] = __ldcg(D.sum_topk + (size_t)(q0 + i) * K + j);
+        }
+        __syncwarp();
+        ScanIn in{D.cfg, D.C, (long long)D.V, D.d, cum_s - q0, Uo_s - q0, lrh_s - q0, lse_s - q0, min_s - q0,
+                  max_s - q0, topk_s - (size_t)q0 * k, k, D.S_logits};
+        Scan<WarpPrims> sc{in, st, run, run_alt, prims, res};
+        sc.run(q1);
+        __syncwarp();
+        q0 = q1;
+    }
     st.iter += 1;
+    if (lane == 0) DBG_TS(D, 20 + 8 * (st0.iter & 1));
     for (int i = lane; i < st.kcount; i += 32) D.run_a[i] = run[i];
     if (st.phase == PH_DONE) {
         if (lane == 0) {
@@ -644,7 +704,9 @@ __device__ __noinline__ void run_scan(const Dev &D, const ScanState &st0, double
             set_cond(D, 1);
         }
     } else {  // need more clusters: plan the next wave (all lanes, identical)
-        int hi = csvd_plan_wave(st, in);
+        ScanIn gin{D.cfg, D.C, (long long)D.V, D.d, D.cum, D.Uo, D.lrh, nullptr, nullptr, nullptr, nullptr, K,
+                   nullptr};
+        int hi = csvd_plan_wave(st, gin, WarpSearch{});
         start_wave(D, st, hi);
         st.wave_tokens = st.wave_tokens * 2 < D.V ? st.wave_tokens * 2 : (int)D.V;
         for (int q = st.p_lo + lane; q < st.p_hi; q += 32) D.cl_done[q] = 0;
@@ -655,6 +717,7 @@ __device__ __noinline__ void run_scan(const Dev &D, const ScanState &st0, double
         }
     }
     __threadfence();
+    if (lane == 0) DBG_TS(D, 21 + 8 * (st0.iter & 1));
 }
 
 template <typename ET, int CPL, int Q>
@@ -674,6 +737,7 @@ __device__ void wave_sparse(const Dev &D, const ScanState &st0, double *hs, doub
         const int off = r - __ldg(D.cum + q);
         const int pos = __ldg(D.starts + c) + off;
         double logit = row_logit<ET, CPL, Q>(D, pos, hs, scratch, lane);
+        if (gwarp == 0 && lane == 0) DBG_TS(D, 22 + 8 * (st0.iter & 1));
         int last = 0;
         if (lane == 0) {
             D.S_logits[r] = logit;
@@ -694,6 +758,7 @@ __device__ void wave_sparse(const Dev &D, const ScanState &st0, double *hs, doub
             }
             final_ = __shfl_sync(CSVD_FULL, final_, 0);
             if (final_) {
+                if (lane == 0) DBG_TS(D, 18 + 8 * (st0.iter & 1));
                 __threadfence();
                 // all rows of the wave are done -> no other warp of this CTA
                 // still reads hs; reuse shared memory for the scan
@@ -751,8 +816,8 @@ __device__ void wave_dense(const Dev &D, const ScanState &st0, double *hs, doubl
         ScanState st = st0;
         csvd_result res;
         memset(&res, 0, sizeof(res));
-        ScanIn in{D.cfg, D.C, (long long)D.V, D.d, D.order, D.cum, D.U, D.lrh, nullptr, nullptr, nullptr,
-                  nullptr, D.K, nullptr};
+        ScanIn in{D.cfg, D.C, (long long)D.V, D.d, D.cum, D.Uo, D.lrh, nullptr, nullptr, nullptr, nullptr, D.K,
+                  nullptr};
         double *dummy = nullptr;
         WarpPrims prims{0, nullptr};
         Scan<WarpPrims> sc{in, st, dummy, dummy, prims, res};
@@ -806,6 +871,9 @@ struct csvd_ctx {
     cudaGraphExec_t g_step = nullptr, g_bounds = nullptr, g_dense = nullptr;
     cudaGraphConditionalHandle h_step = 0, h_bounds = 0, h_dense = 0;
     int last_launches = 0;
+    int direct = 0;               // 1: launch kernels one by one (profiling / ncu)
+    void *flush_buf = nullptr;
+    ScanState *st_pin = nullptr;
     // host copies of plan tables
     std::vector<int2> wleaves, bleaves;
     std::vector<short> wprog, bprog;
@@ -932,21 +1000,18 @@ extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
     CK(cudaStreamSynchronize(ctx->stream));
     int rc = alloc_k(ctx, K);
     if (rc) return rc;
-    size_t need = sizeof(double) * 3 * (size_t)K;
-    if (need > ctx->smem_wave) {
-        ctx->smem_wave = need;
-    }
     return build_graphs(ctx);
 }
 
 static size_t bounds_smem(const Dev &D) {
-    size_t a = sizeof(double) * ((size_t)D.bd + WARPS * (CSVD_MAX_LEAVES / 4));
-    size_t b = sizeof(double) * (size_t)D.cpad + sizeof(int) * (size_t)D.cpad;
+    size_t a = sizeof(double) * ((size_t)D.bd + (D.bplan.regular ? 0 : WARPS * (CSVD_MAX_LEAVES / 4)));
+    size_t b = 12 * (2 * (size_t)D.cpad + 1) + 16;
     return a > b ? a : b;
 }
 static size_t wave_smem(const Dev &D) {
-    size_t a = sizeof(double) * ((size_t)D.d + WARPS * (CSVD_MAX_LEAVES / 4));
-    size_t b = sizeof(double) * 3 * (size_t)D.K;
+    size_t a = sizeof(double) * ((size_t)D.d + (D.wplan.regular ? 0 : WARPS * (CSVD_MAX_LEAVES / 4)));
+    // scan: two running lists + at least one chunk row of (k + 6) doubles
+    size_t b = sizeof(double) * (2 * (size_t)D.K + 8 + 4 * ((size_t)D.K + 6));
     return a > b ? a : b;
 }
 
@@ -999,8 +1064,10 @@ static int capture_graph(csvd_ctx *ctx, int mode /*0 step,1 bounds,2 dense*/, cu
                          cudaGraphConditionalHandle *hout) {
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    // (a conditional handle that no conditional node uses makes instantiation
+    // fail, so the bounds-only graph has none)
+    cudaGraphConditionalHandle h = 0;
+    if (mode != 1) CK(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
     Dev D = ctx->D;
     D.loop = h;
     D.use_graph = (mode != 1);
@@ -1053,6 +1120,7 @@ static int build_graphs(csvd_ctx *ctx) {
     ctx->smem_bounds = bounds_smem(D);
     size_t ws = wave_smem(D);
     if (ws > ctx->smem_wave) ctx->smem_wave = ws;
+    D.scan_smem_doubles = (int)(ctx->smem_wave / sizeof(double));
     CK(cudaFuncSetAttribute((const void *)bounds_kernel(D), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ctx->smem_bounds));
     CK(cudaFuncSetAttribute((const void *)wave_kernel(D), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1184,6 +1252,7 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     if ((rc = dalloc(ctx, &ctx->d_cfg, 1))) return rc;
     D.cfg = ctx->d_cfg;
     if ((rc = dalloc(ctx, &D.U, C))) return rc;
+    if ((rc = dalloc(ctx, &D.Uo, C))) return rc;
     if ((rc = dalloc(ctx, &D.X, C))) return rc;
     if ((rc = dalloc(ctx, &D.dots, C))) return rc;
     if ((rc = dalloc(ctx, &D.order, C))) return rc;
@@ -1199,6 +1268,11 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     if ((rc = dalloc(ctx, &D.res, 1))) return rc;
     if ((rc = dalloc(ctx, &D.counters, 4))) return rc;
     CK(cudaMemset(D.counters, 0, 16));
+    D.dbg = nullptr;
+    if (getenv("CSVD_DEBUG_TS") && atoi(getenv("CSVD_DEBUG_TS")) > 0) {
+        if ((rc = dalloc(ctx, &D.dbg, 64))) return rc;
+        CK(cudaMemset(D.dbg, 0, 64 * 8));
+    }
     CK(cudaMemset(D.cl_done, 0, sizeof(int) * C));
     CK(cudaMemset(D.st, 0, sizeof(ScanState)));
     CK(cudaMemset(D.res, 0, sizeof(csvd_result)));
@@ -1208,6 +1282,7 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     ctx->smem_bounds = bounds_smem(D);
     D.K = 16;
     ctx->smem_wave = wave_smem(D);
+    D.scan_smem_doubles = (int)(ctx->smem_wave / sizeof(double));
     CK(cudaFuncSetAttribute((const void *)bounds_kernel(D), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ctx->smem_bounds));
     CK(cudaFuncSetAttribute((const void *)wave_kernel(D), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1225,6 +1300,7 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     CK(cudaHostAlloc(&ctx->h_pin, sizeof(double) * (D.d + 1), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->cfg_pin, sizeof(csvd_config), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->res_pin, sizeof(csvd_result), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->st_pin, sizeof(ScanState), cudaHostAllocDefault));
     ctx->pin_cap = V;
     CK(cudaHostAlloc(&ctx->ids_pin, sizeof(long long) * V, cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->logits_pin, sizeof(double) * V, cudaHostAllocDefault));
@@ -1242,9 +1318,11 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     for (void *p : ctx->dev_allocs) cudaFree(p);
     for (int i = 0; i < 6; ++i)
         if (ctx->k_buffers[i]) cudaFree(ctx->k_buffers[i]);
+    if (ctx->flush_buf) cudaFree(ctx->flush_buf);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     if (ctx->cfg_pin) cudaFreeHost(ctx->cfg_pin);
     if (ctx->res_pin) cudaFreeHost(ctx->res_pin);
+    if (ctx->st_pin) cudaFreeHost(ctx->st_pin);
     if (ctx->ids_pin) cudaFreeHost(ctx->ids_pin);
     if (ctx->logits_pin) cudaFreeHost(ctx->logits_pin);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1264,6 +1342,32 @@ static int check_cfg(csvd_ctx *ctx, const csvd_config *cfg) {
     return 0;
 }
 
+// Direct mode: the same kernels without the graph; the host reads the device
+// state after every wave (profiling: ncu cannot see inside conditional nodes).
+static int run_direct(csvd_ctx *ctx, cudaStream_t s, int dense_only) {
+    Dev D = ctx->D;
+    D.use_graph = 0;
+    D.bounds_only = 0;
+    D.dense_only = dense_only;
+    void *args[] = {&D};
+    if (dense_only)
+        CK(cudaLaunchKernel((const void *)k_dense_setup, dim3(1), dim3(32), args, 0, s));
+    else
+        CK(cudaLaunchKernel((const void *)bounds_kernel(D), dim3(ctx->grid_bounds), dim3(THREADS), args,
+                            ctx->smem_bounds, s));
+    int launches = 1;
+    for (int it = 0; it < D.C + 16; ++it) {
+        CK(cudaMemcpyAsync(ctx->st_pin, D.st, sizeof(ScanState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->st_pin->mode == MODE_IDLE) break;
+        CK(cudaLaunchKernel((const void *)wave_kernel(D), dim3(ctx->grid_wave), dim3(THREADS), args, ctx->smem_wave,
+                            s));
+        launches++;
+    }
+    ctx->last_launches = launches;
+    return 0;
+}
+
 static int run_step_async(csvd_ctx *ctx, const csvd_config *cfg, cudaStream_t s) {
     if (!ctx->D.W) return fail(ctx, CSVD_ECONFIG, "bounds-only context (no table)");
     int rc = check_cfg(ctx, cfg);
@@ -1273,7 +1377,14 @@ static int run_step_async(csvd_ctx *ctx, const csvd_config *cfg, cudaStream_t s)
     }
     *ctx->cfg_pin = *cfg;
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    if (ctx->direct) return run_direct(ctx, s, 0);
     CK(cudaGraphLaunch(ctx->g_step, s));
+    return 0;
+}
+
+extern "C" int csvd_set_direct(csvd_ctx *ctx, int32_t direct) {
+    if (!ctx) return CSVD_ESTATE;
+    ctx->direct = direct ? 1 : 0;
     return 0;
 }
 
@@ -1365,6 +1476,7 @@ static int dense_async(csvd_ctx *ctx, cudaStream_t s) {
     cfg.k_max = ctx->D.V;
     *ctx->cfg_pin = cfg;
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    if (ctx->direct) return run_direct(ctx, s, 1);
     CK(cudaGraphLaunch(ctx->g_dense, s));
     return 0;
 }
@@ -1405,9 +1517,50 @@ extern "C" int csvd_info(csvd_ctx *ctx, int64_t *V, int64_t *d, int32_t *C, int3
     return 0;
 }
 
+extern "C" int csvd_debug_timestamps(csvd_ctx *ctx, unsigned long long *out64) {
+    if (!ctx || !ctx->D.dbg) return CSVD_ESTATE;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out64, ctx->D.dbg, 64 * 8, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+extern "C" int csvd_stream(csvd_ctx *ctx, void **stream) {
+    if (!ctx || !stream) return CSVD_ESTATE;
+    *stream = (void *)ctx->stream;
+    return 0;
+}
+
 extern "C" int csvd_last_launches(csvd_ctx *ctx, int32_t *n) {
     if (!ctx || !n) return CSVD_ESTATE;
-    *n = 1 + ctx->res_pin->waves;
+    *n = ctx->direct ? ctx->last_launches : 1 + ctx->res_pin->waves;
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// L2 flush for benchmarking: stream-read a buffer larger than L2 (clean lines,
+// nothing to write back when the next step allocates)
+// ---------------------------------------------------------------------------
+__global__ void k_l2_flush(const uint4 *buf, size_t n, unsigned *sink) {
+    unsigned acc = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint4 v = __ldcg(buf + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9e3779b9u) *sink = acc;  // keep the loads alive
+}
+
+extern "C" int csvd_l2_flush(csvd_ctx *ctx, void *stream) {
+    if (!ctx) return CSVD_ESTATE;
+    cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+    CK(cudaSetDevice(ctx->device));
+    const size_t bytes = 384ull << 20;
+    if (!ctx->flush_buf) {
+        CK(cudaMalloc(&ctx->flush_buf, bytes + 64));
+        CK(cudaMemset(ctx->flush_buf, 1, bytes));
+    }
+    k_l2_flush<<<ctx->grid_wave, 256, 0, s>>>((const uint4 *)ctx->flush_buf, bytes / 16,
+                                               (unsigned *)((char *)ctx->flush_buf + bytes));
+    CK(cudaGetLastError());
     return 0;
 }
 
@@ -1433,8 +1586,8 @@ struct HostPrims {
 
 // Runs the full scan on host given all per-cluster summaries (all C available).
 // Returns 0 and fills res / *p_final / *phase_final.
-extern "C" int csvd_test_scan_host(const csvd_config *cfg, int C, long long V, int d, const int *order, const int *cum,
-                                   const double *U, const double *lrh, const double *sum_lse, const double *sum_min,
+extern "C" int csvd_test_scan_host(const csvd_config *cfg, int C, long long V, int d, const int *cum,
+                                   const double *Uo, const double *lrh, const double *sum_lse, const double *sum_min,
                                    const double *sum_max, const double *sum_topk, int K, const double *S_logits,
                                    int p_sel, csvd_result *res, int *p_final, int *phase_final) {
     ScanState st;
@@ -1447,7 +1600,10 @@ extern "C" int csvd_test_scan_host(const csvd_config *cfg, int C, long long V, i
     HostPrims prims;
     csvd_result r;
     memset(&r, 0, sizeof(r));
-    ScanIn in{cfg, C, V, d, order, cum, U, lrh, sum_lse, sum_min, sum_max, sum_topk, K, S_logits};
+    ScanIn in{cfg, C, V, d, cum, Uo, lrh, sum_lse, sum_min, sum_max, sum_topk, K, S_logits};
+    ScalarSearch search;
+    if (cfg->variant == CSVD_VARIANT_BATCHSELECT) st.p_sel = csvd_select_prefix(in, cfg->k_max, search);
+    if (p_sel > 0 && p_sel != st.p_sel) return -100;  // selection restatement mismatch
     Scan<HostPrims> sc{in, st, ra, rb, prims, r};
     sc.run(C);
     *res = r;

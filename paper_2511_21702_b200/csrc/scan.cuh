@@ -67,12 +67,9 @@ struct ScanState {
 
 CSVD_HD inline double csvd_neg_inf() { return -INFINITY; }
 
-// loads of data written by other warps/CTAs in the same kernel go through L2
-#ifdef __CUDA_ARCH__
-#define CSVD_LD(p) __ldcg(p)
-#else
+// the scan reads its inputs from arrays the executor staged (shared memory
+// on the device, plain arrays on the host)
 #define CSVD_LD(p) (*(p))
-#endif
 
 // np.logaddexp (numpy npy_logaddexp): x==y -> x + log(2); else max + log1p(exp(-|x-y|))
 CSVD_HD inline double csvd_logaddexp(double x, double y) {
@@ -89,9 +86,8 @@ struct ScanIn {
     int C;
     long long V;
     int d;           // hidden dim (flops)
-    const int *order;    // [C]
     const int *cum;      // [C+1] prefix token counts in opening order
-    const double *U;     // [C] bounds by cluster id
+    const double *Uo;    // [C] bounds in opening order (Uo[p] = U[order[p]])
     const double *lrh;   // [C+1] log R-hat after p opens
     const double *sum_lse, *sum_min, *sum_max;  // [C] by opening position
     const double *sum_topk;                      // [C * K] by opening position
@@ -112,9 +108,9 @@ struct Scan {
     P &prims;
     csvd_result &res;
 
-    CSVD_HD double u_at(int p) const { return p >= in.C ? csvd_neg_inf() : in.U[in.order[p]]; }
+    CSVD_HD double u_at(int p) const { return p >= in.C ? csvd_neg_inf() : in.Uo[p]; }
     CSVD_HD long long n_s() const { return in.cum[st.p]; }
-    CSVD_HD double kth() const {
+    CSVD_HD double kth() const {  // the k-th largest computed logit (certify.py:85-88)
         int k = in.cfg->k;
         return st.kcount >= k && n_s() >= k ? lst[k - 1] : csvd_neg_inf();
     }
@@ -300,35 +296,67 @@ struct Scan {
 
 // ---------------------------------------------------------------------------
 // wave planning (speculative opening; never changes results, only how many
-// clusters' logits are computed per device iteration)
+// clusters' logits are computed per device iteration).  All searches are over
+// monotone predicates, so a scalar binary search (host, single thread) and a
+// warp-parallel 32-ary search (device) return the same index.
 // ---------------------------------------------------------------------------
-CSVD_HD inline int csvd_first_prefix_exceeding(const int *cum, int C, long long tokens) {
-    // smallest p in [1, C] with cum[p] > tokens, or C+1 if none
-    int lo = 1, hi = C + 1;
-    while (lo < hi) {
-        int mid = (lo + hi) / 2;
-        if ((long long)cum[mid] > tokens) hi = mid; else lo = mid + 1;
+struct ScalarSearch {
+    // first i in [lo, hi) with pred(i) true, or hi
+    template <class F>
+    CSVD_HD int operator()(int lo, int hi, const F &pred) const {
+        while (lo < hi) {
+            int mid = lo + (hi - lo) / 2;
+            if (pred(mid)) hi = mid; else lo = mid + 1;
+        }
+        return lo;
     }
-    return lo;
+};
+
+// batch-select budget prefix (_select_by_bound, decode.py:346-359):
+// the largest p with cum[p] <= k_max, at least 1
+template <class S>
+CSVD_HD inline int csvd_select_prefix(const ScanIn &in, long long k_max, const S &search) {
+    int p = search(1, in.C + 1, [&](int q) { return (long long)in.cum[q] > k_max; }) - 1;
+    return p < 1 ? 1 : p;
+}
+
+// prefixes never needed: past the budget trigger plus every partial expansion
+template <class S>
+CSVD_HD inline int csvd_cap_prefix(const ScanIn &in, int p_sel, const S &search) {
+    const csvd_config &cfg = *in.cfg;
+    int sum_dc = 0;
+    for (int l = 0; l < cfg.n_levels; ++l)
+        if (cfg.level_kind[l] == CSVD_FB_PARTIAL_EXPAND) sum_dc += (int)cfg.level_param[l];
+    int base;
+    if (cfg.variant == CSVD_VARIANT_BATCHSELECT) {
+        base = p_sel;
+    } else {  // first prefix whose token count exceeds k_max
+        base = search(1, in.C + 1, [&](int q) { return (long long)in.cum[q] > cfg.k_max; });
+        if (base > in.C) base = in.C;
+    }
+    long long cap = (long long)base + sum_dc;
+    return cap > in.C ? in.C : (int)cap;
 }
 
 // Next wave end for phase MAIN / PE.  Returns p_hi > st.p.
-CSVD_HD inline int csvd_plan_wave(const ScanState &st, const ScanIn &in) {
+template <class S>
+CSVD_HD inline int csvd_plan_wave(const ScanState &st, const ScanIn &in, const S &search) {
     if (st.phase == PH_PE) return st.pe_target;
     if (in.cfg->variant == CSVD_VARIANT_BATCHSELECT && st.p < st.p_sel) return st.p_sel;
-    const int base = in.cum[st.p];
-    int hi = csvd_first_prefix_exceeding(in.cum, in.C, (long long)base + st.wave_tokens - 1);
+    const long long want = (long long)in.cum[st.p] + st.wave_tokens;
+    int hi = search(st.p + 1, in.C + 1, [&](int q) { return (long long)in.cum[q] >= want; });
     if (hi > in.C) hi = in.C;
     bool has_topk = false;
     for (int t = 0; t < in.cfg->n_targets; ++t) has_topk = has_topk || in.cfg->targets[t] == CSVD_TARGET_TOPK;
     if (has_topk) {
-        // bound-based extension: clusters whose bound still beats the estimate
-        // of the best logit cannot be excluded by a top-k certificate
-        while (hi < in.C && hi < st.p + 64 && in.U[in.order[hi]] >= st.est) hi++;
+        // clusters whose bound still beats the estimate of the best logit cannot
+        // be excluded by a top-k certificate (Uo is non-increasing)
+        int lim = st.p + 64 < in.C ? st.p + 64 : in.C;
+        if (hi < lim) hi = search(hi, lim, [&](int q) { return in.Uo[q] < st.est; });
     } else {
         // rho(p) >= Rhat(p)/Rhat(0): prefixes with Rhat(p)/Rhat(0) > eps cannot certify
         const double le = log(in.cfg->epsilon);
-        while (hi < in.C && CSVD_SUB(in.lrh[hi], in.lrh[0]) > le) hi++;
+        if (hi < in.C) hi = search(hi, in.C, [&](int q) { return !(CSVD_SUB(in.lrh[q], in.lrh[0]) > le); });
     }
     if (hi > st.p_cap) hi = st.p_cap;
     if (hi <= st.p) hi = st.p + 1;

@@ -25,7 +25,8 @@ def test_decode_matches_reference_goldens(name):
     for st in case.steps():
         fn = P.decode_step if st["variant"] == "incremental" else P.decode_step_batchselect
         out = fn(T, ix, st["h"], st["cfg"], k_max=st["k_max"])
-        assert_outcome(out, case.expected(st["i"]), rtol=TRANS_RTOL, where=f"{name}[{st['i']}]")
+        assert_outcome(out, case.expected(st["i"]), rtol=TRANS_RTOL, where=f"{name}[{st['i']}]",
+                       exact_bounds=ix.mode != "spherical")
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -45,7 +46,10 @@ def test_bounds_match_reference_goldens(name):
         else:
             assert np.array_equal(b.values, exp["U"]), f"{name}: bounds not bit-equal"
         assert b.query_norm == exp["qn"]
-        assert b.slack == exp["slack"]
+        if ix.mode == "spherical":
+            assert abs(b.slack - exp["slack"]) <= 1e-12 * abs(exp["slack"])
+        else:
+            assert b.slack == exp["slack"]
 
 
 @pytest.mark.parametrize("name", golden_names())

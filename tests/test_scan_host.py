@@ -86,9 +86,10 @@ def test_host_scan_matches_reference(name):
         res = _lib.Result()
         pf = ctypes.c_int()
         ph = ctypes.c_int()
-        args = [np.ascontiguousarray(a) for a in (order, cum, U, lrh, lse, mn, mx, topk, S)]
-        rc = lib.csvd_test_scan_host(ctypes.byref(c), C, V, d, *[a.ctypes.data for a in args[:8]], K,
-                                     args[8].ctypes.data, p_sel, ctypes.byref(res), ctypes.byref(pf),
+        Uo = np.ascontiguousarray(U[order])
+        args = [np.ascontiguousarray(a) for a in (cum, Uo, lrh, lse, mn, mx, topk, S)]
+        rc = lib.csvd_test_scan_host(ctypes.byref(c), C, V, d, *[a.ctypes.data for a in args[:7]], K,
+                                     args[7].ctypes.data, p_sel, ctypes.byref(res), ctypes.byref(pf),
                                      ctypes.byref(ph))
         assert rc == 0
         where = f"{name}[{st['i']}]"
