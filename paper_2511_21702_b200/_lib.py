@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libcsvd_b200.so")
+LIB_PATH = os.environ.get("CSVD_LIB", os.path.join(_HERE, "_build", "libcsvd_b200.so"))
 
 CSVD_MAX_LEVELS = 8
 
@@ -139,6 +139,7 @@ def load():
     lib.csvd_set_direct.argtypes = [P, ctypes.c_int32]
     lib.csvd_l2_flush.argtypes = [P, P]
     lib.csvd_test_sizes.argtypes = [P, P, P, P]
+    lib.csvd_debug_timestamps.argtypes = [P, P]
     lib.csvd_test_scan_host.argtypes = [
         ctypes.POINTER(Config), ctypes.c_int, ctypes.c_longlong, ctypes.c_int, P, P, P, P, P, P, P,
         ctypes.c_int, P, ctypes.c_int, ctypes.POINTER(Result), P, P]

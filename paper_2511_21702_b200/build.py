@@ -46,11 +46,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build_extension(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build_extension(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    out = out or OUT
+    if not force and not defines and up_to_date():
         return OUT
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", os.path.join(CSRC, "csvd_b200.cu")]
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp",
+           os.path.join(CSRC, "csvd_b200.cu")]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(OUT_DIR, "ptxas.log")
     with open(log, "w") as f:
@@ -58,10 +60,10 @@ def build_extension(force: bool = False, verbose: bool = False) -> str:
     if proc.returncode != 0:
         sys.stderr.write(proc.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
         print(proc.stderr)
-    return OUT
+    return out
 
 
 def build_oracle() -> str:

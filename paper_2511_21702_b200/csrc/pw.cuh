@@ -150,7 +150,20 @@ template <int CPL> struct NBatch<uint16_t, CPL> { static constexpr int value = 1
 
 // ---------------------------------------------------------------------------
 // REGULAR path: returns 0.0 + pw(row .* h) in every lane
+//
+// h layout in shared memory:
+//  * CPL == 8 (lane = leaf): natural order with a 2-double pad after every
+//    leaf, hs[L*(leaf_len+2) + r] = h[L*leaf_len + r].  A lane reads its 8
+//    values per step as 4 LDS.128; within a quarter-warp the 8 lanes start
+//    4 banks apart ((2*leaf_len+4) mod 32 in {4, 20} for leaf_len % 8 == 0),
+//    so every LDS.128 is conflict-free.
+//  * CPL < 8 (lanes share a leaf): interleaved, hs[((u*S+i)*CPL+c)*32+lane],
+//    built from a host-computed source-index table.
 // ---------------------------------------------------------------------------
+__host__ __device__ inline int pw_hs_size(const PwPlan &pl) {
+    return (pl.regular && pl.cpl == 8) ? pl.n + 2 * pl.nleaf : pl.n;
+}
+
 template <typename ET, int CPL, int Q>
 __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
                                                    const double *__restrict__ hs,
@@ -165,7 +178,8 @@ __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
         const ET *lp = row + (size_t)(u * NLW + lil) * leaf_len + j0;
-        const double *hp = hs + (size_t)u * S * CPL * 32 + lane;
+        const double *hp = (CPL == 8) ? hs + (size_t)(u * 32 + lane) * (leaf_len + 2)
+                                      : hs + (size_t)u * S * CPL * 32 + lane;
         double r[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) r[c] = 0.0;
@@ -178,9 +192,22 @@ __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
             for (int s = 0; s < NB; ++s) {
                 if (i0 + s < S) {
                     const int i = i0 + s;
+                    double hv[CPL];
+                    if constexpr (CPL == 8) {
+                        const double2 *h2 = reinterpret_cast<const double2 *>(hp + 8 * i);
+#pragma unroll
+                        for (int c2 = 0; c2 < 4; ++c2) {
+                            double2 t = h2[c2];
+                            hv[2 * c2] = t.x;
+                            hv[2 * c2 + 1] = t.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) hv[c] = hp[(i * CPL + c) * 32];
+                    }
 #pragma unroll
                     for (int c = 0; c < CPL; ++c) {
-                        double p = d_mul(raw[s].get(c), hp[(i * CPL + c) * 32]);
+                        double p = d_mul(raw[s].get(c), hv[c]);
                         r[c] = (i == 0) ? p : d_add(r[c], p);
                     }
                 }
@@ -211,8 +238,8 @@ __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
     return d_add(0.0, tot);
 }
 
-// index of h element e in the interleaved shared layout of a regular plan
-__device__ __forceinline__ int pw_hs_source(const PwPlan &pl, int idx) {
+// host: source element of interleaved index idx (CPL < 8 plans)
+__host__ __device__ inline int pw_hs_source(const PwPlan &pl, int idx) {
     // idx = ((u*S + i)*CPL + c)*32 + t
     const int t = idx & 31;
     int rest = idx >> 5;
@@ -227,13 +254,27 @@ __device__ __forceinline__ int pw_hs_source(const PwPlan &pl, int idx) {
     return L * pl.leaf_len + 8 * i + j0 + c;
 }
 
-// Stage h (length n_src; element n_src..pl.n-1 -> 1.0 for the bias-augmented
-// [h,1]) into shared memory in the plan's layout.  Block-cooperative.
-__device__ __forceinline__ void pw_stage_h(const PwPlan &pl, const double *__restrict__ h, int n_src,
-                                           double *hs) {
-    for (int idx = threadIdx.x; idx < pl.n; idx += blockDim.x) {
-        int e = pl.regular ? pw_hs_source(pl, idx) : idx;
-        hs[idx] = e < n_src ? h[e] : 1.0;
+// Stage h (length n_src; elements n_src..pl.n-1 are the 1.0 of the
+// bias-augmented [h,1]) into shared memory in the plan's layout.
+// Block-cooperative; loads are independent so they overlap.
+template <int CPL>
+__device__ __forceinline__ void pw_stage(const PwPlan &pl, const double *__restrict__ h, int n_src, double *hs,
+                                         const int *__restrict__ src) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if constexpr (CPL == 8) {
+        const int L = pl.leaf_len;
+        for (int leaf = warp; leaf < pl.nleaf; leaf += nw) {
+            const double *g = h + (size_t)leaf * L;
+            double *t = hs + (size_t)leaf * (L + 2);
+#pragma unroll 4
+            for (int r = lane; r < L; r += 32) t[r] = __ldcg(g + r);
+        }
+    } else if constexpr (CPL > 0) {
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < pl.n; idx += blockDim.x) hs[idx] = __ldcg(h + __ldg(src + idx));
+    } else {
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < pl.n; idx += blockDim.x) hs[idx] = idx < n_src ? __ldcg(h + idx) : 1.0;
     }
 }
 

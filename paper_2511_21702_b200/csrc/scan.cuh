@@ -10,13 +10,15 @@
 //   outcome + tightness              decode.py:212-237, certify.py:172-184
 //
 // Invariant used (verified by tests): the opened set is always a
-// prefix of the bound order, so "u_max over unopened" = U[order[p]] and the
-// residual log R-hat after p opens is the suffix log-sum-exp lrh[p] computed
-// once per step.  The scan consumes per-cluster summaries (top-k values, LSE,
-// min, max) produced by the GEMV epilogue, in opening order, wave by wave;
-// it is run identically by all 32 lanes of one warp on the device (scalar
-// state replicated, collective primitives warp-parallel) and by one thread on
-// the host (unit tests).
+// prefix of the bound order, so "u_max over unopened" = Uo[p] and the residual
+// log R-hat after p opens is the suffix log-sum-exp lrh[p] computed once per
+// step.  Because merges happen in opening order, every per-prefix quantity is a
+// pure function of p: log Z_S(p) (streaming logaddexp, full recompute when
+// p % 64 == 0), the k-th largest logit kth(p), min/max of S, rho(p), delta(p).
+// An executor-supplied precompute fills them for a chunk of prefixes (the host
+// does it sequentially with the reference's exact arithmetic; the device
+// warp-parallel, ulp-close for the transcendental ones and exact for kth /
+// min / max), and the state machine below only compares.
 #pragma once
 #include <cmath>
 #include <cstdint>
@@ -25,8 +27,12 @@
 
 #ifdef __CUDACC__
 #define CSVD_HD __host__ __device__
+// out of line on the device: this code runs once per step with a cold
+// instruction cache, so one shared copy beats many inlined ones
+#define CSVD_HD_NOINL __host__ __device__ __noinline__
 #else
 #define CSVD_HD
+#define CSVD_HD_NOINL
 #endif
 
 enum { PH_MAIN = 0, PH_PE = 1, PH_DONE = 2, PH_DENSE = 3, PH_ERROR = 4 };
@@ -34,7 +40,6 @@ enum { MODE_SPARSE = 0, MODE_DENSE = 1, MODE_IDLE = 2 };
 
 struct ScanState {
     int p;          // clusters merged (opened) so far
-    int merges;
     int kcount;     // entries in the running top-k list
     int phase;
     int level;      // next fallback level index
@@ -44,21 +49,33 @@ struct ScanState {
     int row_lo, row_hi;
     int p_cap;      // never plan beyond this prefix
     int p_sel;      // batchselect selection size
-    int iter;       // wave kernel iterations (guard)
+    int iter;       // wave iterations (guard)
     int mode;       // MODE_*
     int wave_tokens;
     int pad0;
-    double log_z, smin, smax;
+    // values at the current prefix p
+    double log_z, smin, smax, kth, rho, delta;
     double est;     // wave heuristic: lower estimate of the best logit
 };
 
-// Exact helpers with host fallbacks (the host path only runs in unit tests).
+#ifdef __CUDACC__
+__device__ __noinline__ double csvd_ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __noinline__ double csvd_exp(double x) { return exp(x); }
+__device__ __noinline__ double csvd_log(double x) { return log(x); }
+__device__ __noinline__ double csvd_log1p(double x) { return log1p(x); }
+#endif
 #ifdef __CUDA_ARCH__
 #define CSVD_ADD(a, b) __dadd_rn((a), (b))
 #define CSVD_SUB(a, b) __dsub_rn((a), (b))
 #define CSVD_MUL(a, b) __dmul_rn((a), (b))
-#define CSVD_DIV(a, b) __ddiv_rn((a), (b))
+#define CSVD_DIV(a, b) csvd_ddiv((a), (b))
+#define CSVD_EXP(x) csvd_exp(x)
+#define CSVD_LOG(x) csvd_log(x)
+#define CSVD_LOG1P(x) csvd_log1p(x)
 #else
+#define CSVD_EXP(x) exp(x)
+#define CSVD_LOG(x) log(x)
+#define CSVD_LOG1P(x) log1p(x)
 #define CSVD_ADD(a, b) ((a) + (b))
 #define CSVD_SUB(a, b) ((a) - (b))
 #define CSVD_MUL(a, b) ((a) * (b))
@@ -67,17 +84,25 @@ struct ScanState {
 
 CSVD_HD inline double csvd_neg_inf() { return -INFINITY; }
 
-// the scan reads its inputs from arrays the executor staged (shared memory
-// on the device, plain arrays on the host)
-#define CSVD_LD(p) (*(p))
-
 // np.logaddexp (numpy npy_logaddexp): x==y -> x + log(2); else max + log1p(exp(-|x-y|))
 CSVD_HD inline double csvd_logaddexp(double x, double y) {
     if (x == y) return CSVD_ADD(x, 0.69314718055994530942);
     double t = CSVD_SUB(x, y);
-    if (t > 0) return CSVD_ADD(x, log1p(exp(-t)));
-    if (t <= 0) return CSVD_ADD(y, log1p(exp(t)));
+    if (t > 0) return CSVD_ADD(x, CSVD_LOG1P(CSVD_EXP(-t)));
+    if (t <= 0) return CSVD_ADD(y, CSVD_LOG1P(CSVD_EXP(t)));
     return t;  // nan
+}
+
+// certify.CertState.rho / delta (certify.py:93-107) from log Z_S and log R-hat
+CSVD_HD inline double csvd_rho(double log_z, double lr) {
+    if (lr == csvd_neg_inf()) return 0.0;
+    if (log_z == csvd_neg_inf()) return 1.0;
+    return CSVD_DIV(1.0, CSVD_ADD(1.0, CSVD_EXP(CSVD_SUB(log_z, lr))));
+}
+CSVD_HD inline double csvd_delta(double log_z, double lr) {
+    if (lr == csvd_neg_inf()) return 0.0;
+    if (log_z == csvd_neg_inf()) return INFINITY;
+    return CSVD_EXP(CSVD_SUB(lr, log_z));
 }
 
 // Read-only step inputs for the scan.
@@ -85,101 +110,66 @@ struct ScanIn {
     const csvd_config *cfg;
     int C;
     long long V;
-    int d;           // hidden dim (flops)
+    int d;               // hidden dim (flops)
     const int *cum;      // [C+1] prefix token counts in opening order
     const double *Uo;    // [C] bounds in opening order (Uo[p] = U[order[p]])
     const double *lrh;   // [C+1] log R-hat after p opens
-    const double *sum_lse, *sum_min, *sum_max;  // [C] by opening position
-    const double *sum_topk;                      // [C * K] by opening position
-    int K;                                       // top-k row stride
-    const double *S_logits;                      // logits in opening order
 };
 
-// Primitives supplied by the executor (warp on device, thread on host):
-//   merge_topk(run, kr, add, ka, k, out) -> new count (top-k of the union, desc)
-//   lse_all(vals, n, vmax) -> logsumexp over vals[0..n)
-//   writer() -> true for the lane allowed to write memory
-template <class P>
+// Per-prefix values for clusters q in [q0, q1): index i = q - q0 describes
+// prefix p = q + 1.
+struct Chunk {
+    int q0, q1;
+    const double *log_z, *kth, *smin, *smax, *rho, *delta;
+};
+
 struct Scan {
     const ScanIn &in;
     ScanState &st;
-    double *&lst;     // running top-k list (double buffered)
-    double *&lst_alt;
-    P &prims;
     csvd_result &res;
 
     CSVD_HD double u_at(int p) const { return p >= in.C ? csvd_neg_inf() : in.Uo[p]; }
     CSVD_HD long long n_s() const { return in.cum[st.p]; }
-    CSVD_HD double kth() const {  // the k-th largest computed logit (certify.py:85-88)
-        int k = in.cfg->k;
-        return st.kcount >= k && n_s() >= k ? lst[k - 1] : csvd_neg_inf();
-    }
-    CSVD_HD double rho() const {
-        double lr = in.lrh[st.p];
-        if (lr == csvd_neg_inf()) return 0.0;
-        if (st.log_z == csvd_neg_inf()) return 1.0;
-        return CSVD_DIV(1.0, CSVD_ADD(1.0, exp(CSVD_SUB(st.log_z, lr))));
-    }
-    CSVD_HD double delta() const {
-        double lr = in.lrh[st.p];
-        if (lr == csvd_neg_inf()) return 0.0;
-        if (st.log_z == csvd_neg_inf()) return INFINITY;
-        return exp(CSVD_SUB(lr, st.log_z));
-    }
 
-    // CertState.merge_cluster for the cluster at opening position q (== st.p)
-    CSVD_HD void merge(int q) {
-        const int k = in.cfg->k;
-        const int size = in.cum[q + 1] - in.cum[q];
-        const int ka = size < k ? size : k;
-        st.kcount = prims.merge_topk(lst, st.kcount, in.sum_topk + (size_t)q * in.K, ka, k, lst_alt);
-        double *t = lst;
-        lst = lst_alt;
-        lst_alt = t;
-        const double mn = CSVD_LD(in.sum_min + q), mx = CSVD_LD(in.sum_max + q);
-        if (st.p == 0) {
-            st.smin = mn;
-            st.smax = mx;
-        } else {
-            st.smin = mn < st.smin ? mn : st.smin;
-            st.smax = mx > st.smax ? mx : st.smax;
-        }
+    // CertState.merge_cluster of the cluster at opening position q == st.p
+    CSVD_HD void merge(const Chunk &ch, int q) {
+        const int i = q - ch.q0;
         st.p = q + 1;
-        st.merges += 1;
-        if (st.merges % 64 == 0)
-            st.log_z = prims.lse_all(in.S_logits, in.cum[st.p], st.smax);
-        else
-            st.log_z = csvd_logaddexp(st.log_z, CSVD_LD(in.sum_lse + q));
+        st.log_z = ch.log_z[i];
+        st.kth = ch.kth[i];
+        st.smin = ch.smin[i];
+        st.smax = ch.smax[i];
+        st.rho = ch.rho[i];
+        st.delta = ch.delta[i];
     }
 
     // check_targets (decode.py:192-210); returns true and fills res when certified
-    CSVD_HD bool check(double eps, int fb) {
+    CSVD_HD_NOINL bool check(double eps, int fb) {
         const csvd_config &cfg = *in.cfg;
         const long long n = n_s();
         for (int ti = 0; ti < cfg.n_targets; ++ti) {
             int t = cfg.targets[ti];
             if (t == CSVD_TARGET_TOPK) {
                 if (n < cfg.k) continue;
-                double kth_v = kth();
-                if (st.p >= in.C) return finish(CSVD_KIND_TOPK_EXACT, 0.0, csvd_neg_inf(), kth_v, fb);
+                if (st.p >= in.C) return finish(CSVD_KIND_TOPK_EXACT, 0.0, csvd_neg_inf(), st.kth, fb);
                 double u = u_at(st.p);
-                if (u < kth_v) return finish(CSVD_KIND_TOPK_EXACT, 0.0, u, kth_v, fb);
+                if (u < st.kth) return finish(CSVD_KIND_TOPK_EXACT, 0.0, u, st.kth, fb);
             } else if (t == CSVD_TARGET_SOFTMAX) {
                 if (n == 0) continue;
-                double r = rho();
-                if (r <= eps) return finish(CSVD_KIND_SOFTMAX_EPS, r, u_at(st.p), kth(), fb);
+                if (st.rho <= eps) return finish(CSVD_KIND_SOFTMAX_EPS, st.rho, u_at(st.p), st.kth, fb);
             } else if (t == CSVD_TARGET_TOPP) {
                 if (n == 0) continue;
-                double dl = delta();
+                double dl = st.delta;
                 double mass = isfinite(dl) ? CSVD_DIV(dl, CSVD_ADD(1.0, dl)) : 1.0;
-                if (dl <= CSVD_DIV(eps, CSVD_SUB(1.0, eps))) return finish(CSVD_KIND_TOPP_MASS, mass, u_at(st.p), kth(), fb);
+                if (dl <= CSVD_DIV(eps, CSVD_SUB(1.0, eps)))
+                    return finish(CSVD_KIND_TOPP_MASS, mass, u_at(st.p), st.kth, fb);
             }
         }
         return false;
     }
 
     // decode._StepContext.outcome (decode.py:212-237) scalars
-    CSVD_HD bool finish(int kind, double eps_ach, double u, double kth_v, int fb) {
+    CSVD_HD_NOINL bool finish(int kind, double eps_ach, double u, double kth_v, int fb) {
         const long long n = n_s();
         double xi;
         if (n < 2 || st.p >= in.C) {
@@ -196,14 +186,14 @@ struct Scan {
         res.epsilon_achieved = eps_ach;
         res.u_max = u;
         res.topk_min = kth_v;
-        res.rho = rho();
+        res.rho = st.rho;
         res.xi = xi;
         st.phase = PH_DONE;
         return true;
     }
 
     // _run_fallback_chain from st.level at prefix st.p (decode.py:268-309).
-    CSVD_HD void run_levels() {
+    CSVD_HD_NOINL void run_levels() {
         const csvd_config &cfg = *in.cfg;
         while (st.level < cfg.n_levels) {
             const int kind = cfg.level_kind[st.level];
@@ -226,16 +216,15 @@ struct Scan {
                 for (int ti = 0; ti < cfg.n_targets; ++ti) {
                     int t = cfg.targets[ti];
                     if (t == CSVD_TARGET_SOFTMAX) {
-                        double r = rho();
-                        if (r <= relaxed) {
-                            finish(CSVD_KIND_SOFTMAX_EPS, r, u_at(st.p), kth(), CSVD_FB_RELAX_EPS);
+                        if (st.rho <= relaxed) {
+                            finish(CSVD_KIND_SOFTMAX_EPS, st.rho, u_at(st.p), st.kth, CSVD_FB_RELAX_EPS);
                             return;
                         }
                     } else if (t == CSVD_TARGET_TOPP) {
-                        double dl = delta();
+                        double dl = st.delta;
                         double mass = isfinite(dl) ? CSVD_DIV(dl, CSVD_ADD(1.0, dl)) : 1.0;
                         if (dl <= CSVD_DIV(relaxed, CSVD_SUB(1.0, relaxed))) {
-                            finish(CSVD_KIND_TOPP_MASS, mass, u_at(st.p), kth(), CSVD_FB_RELAX_EPS);
+                            finish(CSVD_KIND_TOPP_MASS, mass, u_at(st.p), st.kth, CSVD_FB_RELAX_EPS);
                             return;
                         }
                     }
@@ -249,11 +238,11 @@ struct Scan {
         st.phase = PH_DENSE;  // FullVocab is always the implicit last level
     }
 
-    // Consume clusters [st.p, avail) in opening order.
-    CSVD_HD void run(int avail) {
+    // Consume the chunk's clusters in opening order.
+    CSVD_HD void run(const Chunk &ch) {
         const csvd_config &cfg = *in.cfg;
-        while (st.p < avail && (st.phase == PH_MAIN || st.phase == PH_PE)) {
-            merge(st.p);
+        while (st.p < ch.q1 && (st.phase == PH_MAIN || st.phase == PH_PE)) {
+            merge(ch, st.p);
             if (st.phase == PH_MAIN) {
                 if (cfg.variant == CSVD_VARIANT_INCREMENTAL) {
                     st.heap_pops = st.p;
@@ -297,7 +286,7 @@ struct Scan {
 // ---------------------------------------------------------------------------
 // wave planning (speculative opening; never changes results, only how many
 // clusters' logits are computed per device iteration).  All searches are over
-// monotone predicates, so a scalar binary search (host, single thread) and a
+// monotone predicates, so a scalar binary search (host / one thread) and a
 // warp-parallel 32-ary search (device) return the same index.
 // ---------------------------------------------------------------------------
 struct ScalarSearch {
@@ -355,7 +344,7 @@ CSVD_HD inline int csvd_plan_wave(const ScanState &st, const ScanIn &in, const S
         if (hi < lim) hi = search(hi, lim, [&](int q) { return in.Uo[q] < st.est; });
     } else {
         // rho(p) >= Rhat(p)/Rhat(0): prefixes with Rhat(p)/Rhat(0) > eps cannot certify
-        const double le = log(in.cfg->epsilon);
+        const double le = CSVD_LOG(in.cfg->epsilon);
         if (hi < in.C) hi = search(hi, in.C, [&](int q) { return !(CSVD_SUB(in.lrh[q], in.lrh[0]) > le); });
     }
     if (hi > st.p_cap) hi = st.p_cap;

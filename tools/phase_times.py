@@ -18,24 +18,32 @@ ctx = P.prepare(T, ix)
 lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
-names = {0: "bounds start", 1: "h staged", 2: "qnorm", 3: "cta0 rows done", 4: "last cta start",
-         5: "slack/keys", 6: "sorted", 7: "scans", 8: "published", 9: "bounds end",
-         16: "wave0 start", 17: "wave0 h staged", 22: "wave0 first row", 18: "wave0 final summary",
-         19: "wave0 scan start", 20: "wave0 scan end", 21: "wave0 planned",
-         24: "wave1 start", 25: "wave1 staged", 30: "wave1 first row", 26: "wave1 final", 27: "wave1 scan start",
-         28: "wave1 scan end", 29: "wave1 planned"}
+names = {0: "kernel start", 1: "h staged", 2: "cta0 bounds done", 3: "barrier1 passed",
+         4: "rank done (cta0)", 5: "barrier2 passed", 6: "ordering loaded + planned"}
+for w in range(4):
+    names.update({8 + 4 * w: f"wave{w} rows start", 9 + 4 * w: f"wave{w} barrier passed",
+                  10 + 4 * w: f"wave{w} summaries done", 11 + 4 * w: f"wave{w} scan+plan done"})
 for i, h in enumerate(q):
-    buf = np.zeros(64, dtype=np.uint64)
+    buf = np.zeros(128, dtype=np.uint64)
     import ctypes as C_
-    lib.csvd_l2_flush(ctx._ctx, None)
+    if not os.environ.get("NOFLUSH"):
+        lib.csvd_l2_flush(ctx._ctx, None)
     out = ctx.step(h, ctx.make_config(cfg))
     lib.csvd_debug_timestamps(ctx._ctx, buf.ctypes.data)
     if i < 2:
         continue
     t0 = int(buf[0])
-    print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves}")
+    print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} fb={out.fallback_used}")
+    prev = None
     for slot in sorted(names, key=lambda s: int(buf[s]) if buf[s] else 1 << 62):
         if buf[slot]:
-            print(f"   {names[slot]:>22s}: {(int(buf[slot]) - t0) / 1000:8.2f} us")
+            ghz = ""
+            if prev is not None and buf[64 + slot] and buf[64 + prev] and int(buf[slot]) > int(buf[prev]):
+                dc = int(buf[64 + slot]) - int(buf[64 + prev])
+                dt = int(buf[slot]) - int(buf[prev])
+                if 0 < dc < 1e9:
+                    ghz = f"   {dc / dt:5.2f} cyc/ns over {dc} cyc"
+            print(f"   {names[slot]:>22s}: {(int(buf[slot]) - t0) / 1000:8.2f} us{ghz}")
+            prev = slot
     if i > 4:
         break
