@@ -5,8 +5,9 @@
 #include <cuda_runtime.h>
 template <int N>
 __global__ void straight(float *out, long long *cyc, float a) {
-    float x = a, y = a * 2.f, z = a * 3.f, w = a * 4.f;
-    long long t0 = clock64();
+    long long t0;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0)::"memory");
+    float x = a + (float)(t0 & 1) * 0.f, y = a * 2.f, z = a * 3.f, w = a * 4.f;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         x = x * 1.0001f + y;
@@ -14,7 +15,9 @@ __global__ void straight(float *out, long long *cyc, float a) {
         z = z * 1.0002f + w;
         w = w * 0.9998f + x;
     }
-    long long t1 = clock64();
+    long long t1;
+    float sink = x + y + z + w;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1) : "f"(sink) : "memory");
     if (threadIdx.x == 0) { out[blockIdx.x] = x + y + z + w; cyc[blockIdx.x] = t1 - t0; }
 }
 __global__ void flush(const float4 *b, size_t n, float *o) {
