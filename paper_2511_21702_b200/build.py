@@ -22,9 +22,15 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",            # belt and braces: the kernels use __dmul_rn/__dadd_rn anyway
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
+    "-diag-suppress", "20279",  # extern __global__ templates (kinst.cu instantiates them)
 ]
+
+# step-kernel instantiations: (weight element type, chains per lane, slices);
+# CPL 0 = generic pairwise program (any d)
+KINST = [(et, cpl, q) for et in ("float", "uint16_t")
+         for (cpl, q) in ((8, 1), (8, 2), (8, 4), (4, 1), (2, 1), (1, 1), (0, 0))]
 
 
 def _nvcc() -> str:
@@ -51,18 +57,34 @@ def build_extension(force: bool = False, verbose: bool = False, defines=(), out:
     if not force and not defines and up_to_date():
         return OUT
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp",
-           os.path.join(CSRC, "csvd_b200.cu")]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    odir = os.path.join(OUT_DIR, "obj")
+    os.makedirs(odir, exist_ok=True)
+    defs = [f"-D{d}" for d in defines]
+    jobs = [[_nvcc(), *NVCC_FLAGS, *defs, "-c", "-o", os.path.join(odir, "csvd_b200.o"),
+             os.path.join(CSRC, "csvd_b200.cu")]]
+    for et, cpl, q in KINST:
+        jobs.append([_nvcc(), *NVCC_FLAGS, *defs, f"-DKI_ET={et}", f"-DKI_CPL={cpl}", f"-DKI_Q={q}", "-c",
+                     "-o", os.path.join(odir, f"k_{et}_{cpl}_{q}.o"), os.path.join(CSRC, "kinst.cu")])
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        procs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs))
     log = os.path.join(OUT_DIR, "ptxas.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+        for cmd, proc in zip(jobs, procs):
+            f.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+    for proc in procs:
+        if proc.returncode != 0:
+            sys.stderr.write(proc.stderr)
+            raise RuntimeError(f"nvcc failed (see {log})")
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp",
+            *[c[c.index("-o") + 1] for c in jobs]]
+    proc = subprocess.run(link, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stderr)
-        raise RuntimeError(f"nvcc failed (see {log})")
+        raise RuntimeError("nvcc link failed: " + proc.stderr)
     os.replace(out + ".tmp", out)
     if verbose:
-        print(proc.stderr)
+        print(open(log).read())
     return out
 
 

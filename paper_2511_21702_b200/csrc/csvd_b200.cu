@@ -51,7 +51,7 @@ struct csvd_ctx {
     std::string err;
     cudaStream_t stream = nullptr;
     std::vector<void *> dev_allocs;
-    void *k_buffers[4] = {};  // K-dependent: dense candidate lists
+    void *k_buffers[4] = {};  // K-dependent: dense candidate lists, cluster top-k summaries
     kern_t kern = nullptr;
     int grid = 0;
     int nsm = 0;
@@ -145,6 +145,17 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
 }
 
 // --- kernel instantiation per (weight dtype, W plan, bounds plan) ----------
+// (instantiated in kinst.cu, one translation unit per dtype / plan)
+#define CSVD_EXTERN_K(ET, CPL, Q)                                  \
+    extern template __global__ void k_step<ET, CPL, Q, CPL, Q>(Dev); \
+    extern template __global__ void k_step<ET, CPL, Q, 0, 0>(Dev);
+#define CSVD_EXTERN_ET(ET) \
+    CSVD_EXTERN_K(ET, 8, 1) CSVD_EXTERN_K(ET, 8, 2) CSVD_EXTERN_K(ET, 8, 4) \
+    CSVD_EXTERN_K(ET, 4, 1) CSVD_EXTERN_K(ET, 2, 1) CSVD_EXTERN_K(ET, 1, 1)
+CSVD_EXTERN_ET(float)
+CSVD_EXTERN_ET(uint16_t)
+extern template __global__ void k_step<float, 0, 0, 0, 0>(Dev);
+extern template __global__ void k_step<uint16_t, 0, 0, 0, 0>(Dev);
 template <typename ET, int CPL, int Q>
 static kern_t pick_b(bool same) {
     if (same) return k_step<ET, CPL, Q, CPL, Q>;
@@ -182,9 +193,8 @@ static void layout_smem(csvd_ctx *ctx) {
     D.scratch_off = (int)off;
     if (!D.wplan.regular || !D.bplan.regular) off += WARPS * (CSVD_MAX_LEAVES / 4);
     D.ord_off = (int)off;
-    // rank staging (U, x, e: 3 doubles + |c|: 1 int per cluster) then the
-    // ordering (Uo, lrh: doubles; order, cum: ints)
-    off += (28 * (size_t)D.C + 64) / 8;
+    // the per-CTA ordering (sort keys, U, Uo, lrh; order, cum)
+    off += ord_doubles(D.C, D.Cp);
     off = (off + 1) & ~(size_t)1;
     D.sum_off = (int)off;
     // chunk scratch: 9*CHUNK values + 2 K-lists + chunk*K top-k rows
@@ -207,6 +217,9 @@ static int alloc_k(csvd_ctx *ctx, int K) {
     CK(cudaMalloc(&p, sizeof(double) * nw * K + 16));
     ctx->k_buffers[0] = p;
     D.cand = (double *)p;
+    CK(cudaMalloc(&p, sizeof(double) * (size_t)D.C * K + 16));
+    ctx->k_buffers[1] = p;
+    D.sum_topk = (double *)p;
     D.K = K;
     return 0;
 }
@@ -305,6 +318,9 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     D.V = (int)t->vocab_size;
     D.d = (int)t->hidden_dim;
     D.C = ix->n_clusters;
+    D.Cp = 1;
+    while (D.Cp < D.C) D.Cp <<= 1;
+    if (D.Cp < 2) D.Cp = 2;
     D.mode = ix->mode;
     D.bd = D.d + (ix->mode == CSVD_MODE_BIAS_AUGMENTED ? 1 : 0);
     D.wdtype = t->w_dtype;
@@ -422,10 +438,12 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     D.cfg = ctx->d_cfg;
     if ((rc = dalloc(ctx, &D.U, C))) return rc;
     if ((rc = dalloc(ctx, &D.dots, C))) return rc;
-    if ((rc = dalloc(ctx, &D.Uo, C))) return rc;
-    if ((rc = dalloc(ctx, &D.order, C))) return rc;
-    if ((rc = dalloc(ctx, &D.cum, C + 1))) return rc;
-    if ((rc = dalloc(ctx, &D.lrh, C + 1))) return rc;
+    if ((rc = dalloc(ctx, &D.Uraw, C))) return rc;
+    if ((rc = dalloc(ctx, &D.cnt, C))) return rc;
+    CK(cudaMemset(D.cnt, 0, sizeof(int) * C));
+    if ((rc = dalloc(ctx, &D.sum_lse, C))) return rc;
+    if ((rc = dalloc(ctx, &D.sum_min, C))) return rc;
+    if ((rc = dalloc(ctx, &D.sum_max, C))) return rc;
     if ((rc = dalloc(ctx, &D.S_logits, (size_t)V))) return rc;
     if ((rc = dalloc(ctx, &D.S_ids, (size_t)V))) return rc;
     if ((rc = dalloc(ctx, &D.st, 1))) return rc;
@@ -493,8 +511,10 @@ static int check_cfg(csvd_ctx *ctx, const csvd_config *cfg) {
 // device-side result error -> error code
 static int result_error(csvd_ctx *ctx, const csvd_result &r) {
     if (!r.error) return 0;
+    cudaMemset(&ctx->D.res->error, 0, sizeof(int32_t));
     if (r.error == CSVD_EVALUE) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
     cudaMemset(ctx->D.bar, 0, 16);  // a timed-out barrier leaves stale counts
+    cudaMemset(ctx->D.cnt, 0, sizeof(int) * ctx->D.C);
     return fail(ctx, r.error, "device state error (grid barrier timeout)");
 }
 

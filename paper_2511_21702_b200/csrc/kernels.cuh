@@ -45,7 +45,7 @@
 enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2 };
 
 struct Dev {
-    int V, d, C, bd, mode, wdtype;
+    int V, d, C, Cp, bd, mode, wdtype;  // Cp: C rounded up to a power of two (sort)
     int K;  // top-k capacity (row stride of the dense candidate lists, list buffers)
     const void *W;      // [V, d] permuted rows (fp32 | bf16)
     const float *bias;  // [V] permuted
@@ -58,9 +58,10 @@ struct Dev {
     // per step
     const double *h;         // [d]
     const csvd_config *cfg;
-    double *U, *dots;        // [C] by cluster id (U final, with slack)
-    double *Uo, *lrh;        // [C], [C+1] by opening position
-    int *order, *cum;        // [C], [C+1]
+    double *U, *Uraw, *dots; // [C] by cluster id (U final with slack; Uraw / dots from the bounds phase)
+    int *cnt;                // [C] rows finished per opening position (reset by the summariser)
+    double *sum_topk;        // [C*K] per-position cluster top-k (desc), from the rows phase
+    double *sum_lse, *sum_min, *sum_max;  // [C]
     double *S_logits;        // [V]
     long long *S_ids;        // [V]
     double *cand;            // [nwarps*K] dense per-warp candidates
@@ -149,7 +150,7 @@ __device__ __forceinline__ int warp_isum(int v) {
 
 // (m, s) represents m + log(s); combine is associative up to rounding.
 // Out of line: one copy of the f64 exp code instead of one per call site.
-__device__ __noinline__ void lse_combine(double &m, double &s, double m2, double s2) {
+static __device__ __noinline__ void lse_combine(double &m, double &s, double m2, double s2) {
     if (m2 == -INFINITY) return;
     if (m == -INFINITY) {
         m = m2;
@@ -171,7 +172,7 @@ __device__ __forceinline__ bool key_before(double ua, int ia, double ub, int ib)
 }
 
 // Plain grid barrier (cooperative launch: all CTAs resident).
-__device__ __noinline__ void grid_sync(const Dev &D) {
+static __device__ __forceinline__ void grid_sync(const Dev &D) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned gen = ld_acquire(D.bar + 1);
@@ -264,7 +265,7 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
                 u = __dadd_rn(dot, __dmul_rn(D.radii[c], qn));
             else
                 u = __dadd_rn(__dadd_rn(dot, __dmul_rn(D.radii[c], qn)), D.maxb[c]);
-            D.U[c] = u;  // raw (the rank phase adds the slack)
+            D.Uraw[c] = u;  // the order phase adds the slack
             D.dots[c] = dot;
         }
     }
@@ -272,167 +273,452 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
 }
 
 // ---------------------------------------------------------------------------
-// rank phase (all CTAs): the opening order without a sort
+// order phase (every CTA, redundantly, in shared memory): the opening order
+// np.lexsort((arange(C), -U)) (decode.py:166) by a block bitonic sort, the
+// prefix token counts in that order, and log R-hat after every prefix
+// (certify.py:114-119) by a block suffix scan.  No global round trip and no
+// grid barrier: every CTA ends the phase holding the full ordering.
 // ---------------------------------------------------------------------------
-struct RankShared {
-    double slack, xmax;
-    int c0;   // cluster ranked first
-    int bad;  // non-finite bound seen
+struct Ord {  // the full ordering, per CTA
+    int *order, *cum;      // [C] cluster at each opening position, [C+1] tokens before it
+    double *Uo, *lrh;      // [C] bound at each position, [C+1] log R-hat after p opens
+    unsigned long long *keys;  // [Cp] sort keys (then x = log|c| + U by position)
+    double *Us;            // [C] U + slack by cluster id (then exp(x - xmax) by position)
 };
 
-// Stages U (+slack), x = log|c| + U, e = exp(x - xmax), |c| in shared memory,
-// then every warp ranks its own clusters.  Returns false (in every CTA) if a
-// bound is non-finite.  Predicted first-wave clusters get their W rows
-// prefetched into L2.
-__device__ __noinline__ bool rank_phase(const Dev &D, double *ws, RankShared &rs) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// shared-memory footprint of the ordering region, in doubles (host + device)
+__host__ __device__ inline int ord_doubles(int C, int Cp) {
+    return Cp + C + C + (C + 1) + (Cp + (C + 1) + 2) / 2 + 1;
+}
+
+__device__ __forceinline__ void ord_bind(const Dev &D, double *ws, Ord &o) {
+    const int C = D.C, Cp = D.Cp;
+    o.keys = reinterpret_cast<unsigned long long *>(ws);
+    o.Us = ws + Cp;
+    o.Uo = o.Us + C;
+    o.lrh = o.Uo + C;
+    o.order = reinterpret_cast<int *>(o.lrh + C + 1);
+    o.cum = o.order + Cp;
+}
+
+__device__ __forceinline__ double block_max(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double m = red[0];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) m = fmax(m, red[w]);
+    return m;
+}
+
+// Stage U + slack (bounds.py:58-64, which needs max |U| first) by cluster id
+// in shared memory; CTA 0 publishes it for cluster_bounds (bounds.py:178-184).
+// Returns false (in every CTA) if a bound is non-finite.
+static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) {
+    const int tid = threadIdx.x;
     const int C = D.C;
     const csvd_config &cfg = *D.cfg;
-    double *U_s = ws, *x_s = ws + C, *e_s = ws + 2 * C;
-    int *sz_s = reinterpret_cast<int *>(ws + 3 * C);
     __shared__ double s_red[WARPS];
-    __shared__ int s_ired[WARPS];
-    // --- raw bounds (+ slack, bounds.py:58-64, which needs max |U| first)
+    double *__restrict__ Us = o.Us;
     double amax = 1.0;
     for (int c = tid; c < C; c += THREADS) {
-        const double u = __ldcg(D.U + c);
-        U_s[c] = u;
-        sz_s[c] = D.sizes[c];
+        const double u = __ldcg(D.Uraw + c);
+        Us[c] = u;
         amax = fmax(amax, fabs(u));
     }
     double eta = 0.0;
     if (cfg.slack_f32) {
-        amax = warp_max(amax);
-        if (lane == 0) s_red[warp] = amax;
-        __syncthreads();
-        double m = 1.0;
-        for (int w = 0; w < WARPS; ++w) m = fmax(m, s_red[w]);
-        eta = __dmul_rn(__dmul_rn(4.0, 1.1920928955078125e-07), m);
-        __syncthreads();
+        amax = block_max(amax, s_red);
+        eta = __dmul_rn(__dmul_rn(4.0, 1.1920928955078125e-07), amax);
     }
-    double xm = -INFINITY;
     int bad = 0;
     for (int c = tid; c < C; c += THREADS) {
-        const double u = __dadd_rn(U_s[c], eta);
-        U_s[c] = u;
+        const double u = __dadd_rn(Us[c], eta);
         bad |= !isfinite(u);  // BoundVector.__post_init__ (bounds.py:53-55)
-        const double x = __dadd_rn(D.logsz[c], u);  // certify.py:119 np.log(sizes) + U
-        x_s[c] = x;
-        xm = fmax(xm, x);
+        Us[c] = u;
+        if (blockIdx.x == 0) D.U[c] = u;
     }
-    xm = warp_max(xm);
-    bad = __any_sync(CSVD_FULL, bad);
+    bad = __syncthreads_or(bad);
+    if (blockIdx.x == 0 && tid == 0) D.res->slack = eta;
+    return !bad;
+}
+
+__device__ __forceinline__ unsigned long long okey(double u) {  // ascending key == descending U
+    if (u == 0.0) u = 0.0;  // -0.0 ties +0.0, as in the reference's comparison sort
+    return ~dkey(u);
+}
+__device__ __forceinline__ bool okey_before(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// The head of the opening order (fast path; every CTA): the clusters whose
+// bound is at least the wave estimate of the best logit (the first-wave rule
+// of csvd_plan_wave with a top-k target), always including the top cluster.
+// Every other cluster has a smaller bound, so the head is exactly the prefix
+// [0, n) of np.lexsort((arange(C), -U)) (decode.py:166); it is sorted by one
+// warp in registers.  Also fills order/Uo/cum/lrh at position n (the first
+// cluster after the head: the best remaining bound is all a top-k test at
+// p = n needs).  Returns n, or 0 when the head does not apply (more than 64
+// clusters, or a residual sum too small for the direct form): then the full
+// sort runs instead.
+static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = D.C;
+    const double *__restrict__ Us = o.Us;
+    double *__restrict__ xs = reinterpret_cast<double *>(o.keys);  // x by cluster id
+    __shared__ unsigned long long s_k[WARPS];
+    __shared__ int s_i[WARPS], s_n, s_fail, s_head[64];
+    __shared__ double s_x[WARPS];
+    __shared__ double s_est;
+    // --- top cluster c0
+    unsigned long long bk = ~0ull;
+    int bi = 0x7fffffff;
+    for (int c = tid; c < C; c += THREADS) {
+        const unsigned long long k = okey(Us[c]);
+        if (okey_before(k, c, bk, bi)) {
+            bk = k;
+            bi = c;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, bk, off);
+        const int i2 = __shfl_xor_sync(CSVD_FULL, bi, off);
+        if (okey_before(k2, i2, bk, bi)) {
+            bk = k2;
+            bi = i2;
+        }
+    }
     if (lane == 0) {
-        s_red[warp] = xm;
-        s_ired[warp] = bad;
-    }
-    __syncthreads();
-    double xmax = -INFINITY;
-    bad = 0;
-    for (int w = 0; w < WARPS; ++w) {
-        xmax = fmax(xmax, s_red[w]);
-        bad |= s_ired[w];
+        s_k[warp] = bk;
+        s_i[warp] = bi;
     }
     if (tid == 0) {
-        rs.slack = eta;
-        rs.xmax = xmax;
-        rs.bad = bad;
+        s_n = 0;
+        s_fail = 0;
     }
-    if (bad) return false;
-    for (int c = tid; c < C; c += THREADS) e_s[c] = csvd_exp(__dsub_rn(x_s[c], xmax));
     __syncthreads();
-    // --- rank own clusters: position, tokens before, log R-hat at that position
-    const int stride = gridDim.x * WARPS;
-    int j = 0;
-    for (int c = warp * gridDim.x + blockIdx.x; c < C && j < MAX_PER_WARP; c += stride, ++j) {
-        const double uc = U_s[c];
-        int before = 0, off = 0;
-        double tail = 0.0, tmax = -INFINITY;
-        for (int i = lane; i < C; i += 32) {
-            if (key_before(U_s[i], i, uc, c)) {
-                before += 1;
-                off += sz_s[i];
-            } else {
-                tail = __dadd_rn(tail, e_s[i]);
-                tmax = fmax(tmax, x_s[i]);
+    if (tid == 0) {
+        for (int w = 1; w < WARPS; ++w)
+            if (okey_before(s_k[w], s_i[w], bk, bi)) {
+                bk = s_k[w];
+                bi = s_i[w];
+            }
+        s_i[0] = bi;
+        const double dt = __ldcg(D.dots + bi);  // init_state's estimate of the best logit
+        s_est = (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? dt : __dadd_rn(dt, __ldg(D.meanb + bi));
+    }
+    __syncthreads();
+    const int c0 = s_i[0];
+    const double est = s_est;
+    // --- membership, x = log|c| + U (certify.py:119), best non-head cluster
+    double xm = -INFINITY;
+    bk = ~0ull;
+    bi = 0x7fffffff;
+    for (int c = tid; c < C; c += THREADS) {
+        const double u = Us[c];
+        const double x = __dadd_rn(__ldg(D.logsz + c), u);
+        xs[c] = x;
+        xm = fmax(xm, x);
+        if (u >= est || c == c0) {
+            const int slot = atomicAdd(&s_n, 1);
+            if (slot < 64) s_head[slot] = c;
+        } else {
+            const unsigned long long k = okey(u);
+            if (okey_before(k, c, bk, bi)) {
+                bk = k;
+                bi = c;
             }
         }
-        before = warp_isum(before);
-        off = warp_isum(off);
-        tail = warp_sum(tail);
-        tmax = warp_max(tmax);
-        double lr;
-        if (tail > 1e-280) {
-            lr = __dadd_rn(xmax, csvd_log(tail));
-        } else {  // far below the global max: rescale by the tail's own max
-            double t2 = 0.0;
-            for (int i = lane; i < C; i += 32)
-                if (!key_before(U_s[i], i, uc, c)) t2 = __dadd_rn(t2, csvd_exp(__dsub_rn(x_s[i], tmax)));
-            t2 = warp_sum(t2);
-            lr = __dadd_rn(tmax, csvd_log(t2));
-        }
-        if (lane == 0) {
-            D.order[before] = c;
-            D.Uo[before] = uc;
-            D.cum[before] = off;
-            D.lrh[before] = lr;
-            D.U[c] = uc;
+    }
+    xm = warp_max(xm);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, bk, off);
+        const int i2 = __shfl_xor_sync(CSVD_FULL, bi, off);
+        if (okey_before(k2, i2, bk, bi)) {
+            bk = k2;
+            bi = i2;
         }
     }
-    if (blockIdx.x == 0 && tid == 0) {
-        D.cum[C] = D.V;
-        D.lrh[C] = -INFINITY;
-        D.res->slack = eta;
-    }
-    return true;
-}
-
-// ---------------------------------------------------------------------------
-// per-CTA ordering + scan state in shared memory
-// ---------------------------------------------------------------------------
-struct Ord {  // the full ordering, loaded once per step
-    int *order, *cum;
-    double *Uo, *lrh;
-};
-
-__device__ __forceinline__ void ord_bind(const Dev &D, double *ws, Ord &o) {
-    const int C = D.C;
-    o.Uo = ws;
-    o.lrh = ws + C;
-    o.order = reinterpret_cast<int *>(ws + 2 * C + 1);
-    o.cum = o.order + C;
-}
-
-__device__ void load_ordering(const Dev &D, const Ord &o) {
-    const int C = D.C;
-    for (int i = threadIdx.x; i <= C; i += THREADS) {
-        if (i < C) {
-            o.order[i] = __ldcg(D.order + i);
-            o.Uo[i] = __ldcg(D.Uo + i);
-        }
-        o.cum[i] = __ldcg(D.cum + i);
-        o.lrh[i] = __ldcg(D.lrh + i);
+    __syncthreads();  // s_k / s_i reuse
+    if (lane == 0) {
+        s_k[warp] = bk;
+        s_i[warp] = bi;
+        s_x[warp] = xm;
     }
     __syncthreads();
+    const int n = s_n;
+    if (n > 64) return 0;
+    double xmax = s_x[0];
+    for (int w = 1; w < WARPS; ++w) xmax = fmax(xmax, s_x[w]);
+    // --- residual mass of everything outside the head
+    double rest = 0.0;
+    for (int c = tid; c < C; c += THREADS)
+        if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, csvd_exp(__dsub_rn(xs[c], xmax)));
+    rest = warp_sum(rest);
+    __syncthreads();  // s_x reuse
+    if (lane == 0) s_x[warp] = rest;
+    __syncthreads();
+    if (warp == 0) {
+        double S_rest = 0.0;
+        for (int w = 0; w < WARPS; ++w) S_rest = __dadd_rn(S_rest, s_x[w]);
+        int cn = 0x7fffffff;
+        unsigned long long kn = ~0ull;
+        for (int w = 0; w < WARPS; ++w)
+            if (okey_before(s_k[w], s_i[w], kn, cn)) {
+                kn = s_k[w];
+                cn = s_i[w];
+            }
+        // register bitonic sort of the head: lane holds positions lane, lane + 32
+        int ia = lane < n ? s_head[lane] : 0x7fffffff, ib = lane + 32 < n ? s_head[lane + 32] : 0x7fffffff;
+        unsigned long long ka = ia < C ? okey(Us[ia]) : ~0ull, kb = ib < C ? okey(Us[ib]) : ~0ull;
+#pragma unroll 1
+        for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll 1
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                if (j == 32) {  // a (pos lane) vs b (pos lane+32), ascending (kk == 64)
+                    if (okey_before(kb, ib, ka, ia)) {
+                        const unsigned long long tk = ka;
+                        ka = kb;
+                        kb = tk;
+                        const int ti = ia;
+                        ia = ib;
+                        ib = ti;
+                    }
+                } else {
+                    const bool lower = (lane & j) == 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        unsigned long long &k = h ? kb : ka;
+                        int &i = h ? ib : ia;
+                        const int pos = lane + 32 * h;
+                        const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, k, j);
+                        const int i2 = __shfl_xor_sync(CSVD_FULL, i, j);
+                        const bool up = (pos & kk) == 0;
+                        const bool other_first = okey_before(k2, i2, k, i);
+                        if ((lower == up) ? other_first : !other_first) {
+                            k = k2;
+                            i = i2;
+                        }
+                    }
+                }
+            }
+        }
+        // positions lane (a) and lane + 32 (b): order, Uo, cum, lrh
+        const int sa = lane < n ? __ldg(D.sizes + ia) : 0, sb = lane + 32 < n ? __ldg(D.sizes + ib) : 0;
+        const double ea = lane < n ? csvd_exp(__dsub_rn(xs[ia], xmax)) : 0.0;
+        const double eb = lane + 32 < n ? csvd_exp(__dsub_rn(xs[ib], xmax)) : 0.0;
+        int ca = sa, cb = sb;  // inclusive prefix sums
+        double ra = ea, rb = eb;  // inclusive suffix sums
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int ta = __shfl_up_sync(CSVD_FULL, ca, off), tb = __shfl_up_sync(CSVD_FULL, cb, off);
+            const double ua = __shfl_down_sync(CSVD_FULL, ra, off), ub = __shfl_down_sync(CSVD_FULL, rb, off);
+            if (lane >= off) {
+                ca += ta;
+                cb += tb;
+            }
+            if (lane + off < 32) {
+                ra = __dadd_rn(ra, ua);
+                rb = __dadd_rn(rb, ub);
+            }
+        }
+        const int tot_a = __shfl_sync(CSVD_FULL, ca, 31);
+        const double tot_b = __shfl_sync(CSVD_FULL, rb, 0);
+        int fail = 0;
+        if (lane < n) {
+            o.order[lane] = ia;
+            o.Uo[lane] = Us[ia];
+            o.cum[lane] = ca - sa;
+            const double t = __dadd_rn(S_rest, __dadd_rn(ra, tot_b));
+            fail |= !(t > 1e-280);
+            o.lrh[lane] = __dadd_rn(xmax, csvd_log(t));
+        }
+        if (lane + 32 < n) {
+            o.order[lane + 32] = ib;
+            o.Uo[lane + 32] = Us[ib];
+            o.cum[lane + 32] = tot_a + cb - sb;
+            const double t = __dadd_rn(S_rest, rb);
+            fail |= !(t > 1e-280);
+            o.lrh[lane + 32] = __dadd_rn(xmax, csvd_log(t));
+        }
+        const int cbt = __shfl_sync(CSVD_FULL, cb, 31);
+        if (lane == 0) {
+            o.cum[n] = tot_a + cbt;
+            if (n < C) {
+                o.order[n] = cn;
+                o.Uo[n] = Us[cn];
+                fail |= !(S_rest > 1e-280);
+                o.lrh[n] = __dadd_rn(xmax, csvd_log(S_rest));
+            } else {
+                o.lrh[n] = -INFINITY;
+            }
+        }
+        fail = __any_sync(CSVD_FULL, fail);
+        if (lane == 0) s_fail = fail;
+    }
+    __syncthreads();
+    return s_fail ? 0 : n;
+}
+
+// The full opening order (every CTA): bitonic sort of all C (key, id) pairs,
+// prefix token counts and log R-hat after every prefix (block scans).
+// Consumes Us (reused as exp(x - xmax) by position).
+static __device__ __forceinline__ void order_full(const Dev &D, const Ord &o) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = D.C, Cp = D.Cp;
+    __shared__ double s_red[WARPS];
+    __shared__ int s_ired[WARPS];
+    for (int c = tid; c < Cp; c += THREADS) {
+        o.keys[c] = c < C ? okey(o.Us[c]) : ~0ull;
+        o.order[c] = c < C ? c : 0x7fffffff;
+    }
+    __syncthreads();
+    // --- bitonic sort of (key, id) ascending: (-U, id) order.  The arrays
+    // are held in registers as __restrict__ shared pointers: through the Ord
+    // reference every store would force a reload of the pointers from the stack.
+    {
+        unsigned long long *__restrict__ keys = o.keys;
+        int *__restrict__ ids = o.order;
+        const int half = Cp >> 1;
+#pragma unroll 1
+        for (int kk = 2; kk <= Cp; kk <<= 1) {
+#pragma unroll 1
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < half; i += THREADS) {
+                    const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+                    const unsigned long long ka = keys[lo], kb = keys[hi];
+                    const int ia = ids[lo], ib = ids[hi];
+                    const bool a_after = (ka > kb) || (ka == kb && ia > ib);
+                    if (a_after == ((lo & kk) == 0)) {
+                        keys[lo] = kb;
+                        keys[hi] = ka;
+                        ids[lo] = ib;
+                        ids[hi] = ia;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // --- by position: Uo, x = log|c| + U (certify.py:119), sizes -> cum
+    const int seg = (C + THREADS - 1) / THREADS;
+    const int b0 = min(C, tid * seg), b1 = min(C, b0 + seg);
+    double *x = reinterpret_cast<double *>(o.keys);
+    double xm = -INFINITY;
+    int tsum = 0;
+    for (int p = b0; p < b1; ++p) {
+        const int c = o.order[p];
+        const double u = o.Us[c];
+        o.Uo[p] = u;
+        const double xv = __dadd_rn(__ldg(D.logsz + c), u);
+        x[p] = xv;
+        xm = fmax(xm, xv);
+        tsum += __ldg(D.sizes + c);
+    }
+    // exclusive scan of sizes over positions (segments are thread-contiguous)
+    int incl = tsum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(CSVD_FULL, incl, off);
+        if (lane >= off) incl += t;
+    }
+    xm = warp_max(xm);
+    if (lane == 31) s_ired[warp] = incl;
+    if (lane == 0) s_red[warp] = xm;
+    __syncthreads();
+    int run = incl - tsum;
+    double xmax = -INFINITY;
+    for (int w = 0; w < WARPS; ++w) {
+        if (w < warp) run += s_ired[w];
+        xmax = fmax(xmax, s_red[w]);
+    }
+    double tail = 0.0;  // this thread's e-sum (suffix scan below)
+    for (int p = b0; p < b1; ++p) {
+        o.cum[p] = run;
+        run += __ldg(D.sizes + o.order[p]);
+        const double e = csvd_exp(__dsub_rn(x[p], xmax));
+        o.Us[p] = e;  // Us by id is dead: reuse as e by position
+    }
+    for (int p = b1 - 1; p >= b0; --p) tail = __dadd_rn(tail, o.Us[p]);
+    // suffix scan: sum of e over positions >= p
+    double sinc = tail;  // lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double t = __shfl_down_sync(CSVD_FULL, sinc, off);
+        if (lane + off < 32) sinc = __dadd_rn(sinc, t);
+    }
+    __syncthreads();  // s_red reuse
+    if (lane == 0) s_red[warp] = sinc;
+    __syncthreads();
+    double after = 0.0;  // e-sum of the threads after this one: lanes above + warps above
+    {
+        double up = __shfl_down_sync(CSVD_FULL, sinc, 1);
+        if (lane < 31) after = up;
+    }
+    for (int w = WARPS - 1; w > warp; --w) after = __dadd_rn(after, s_red[w]);
+    int need_rescale = 0;
+    double acc = after;
+    for (int p = b1 - 1; p >= b0; --p) {
+        acc = __dadd_rn(acc, o.Us[p]);
+        if (acc > 1e-280) {
+            o.lrh[p] = __dadd_rn(xmax, csvd_log(acc));
+        } else {
+            need_rescale = 1;
+            o.lrh[p] = -INFINITY;
+        }
+    }
+    if (tid == 0) {
+        o.cum[C] = D.V;
+        o.lrh[C] = -INFINITY;
+    }
+    need_rescale = __syncthreads_or(need_rescale);
+    if (need_rescale) {
+        // far below the global max: rescale each deep suffix by its own max (rare)
+        for (int p = warp; p < C; p += WARPS) {
+            if (o.lrh[p] != -INFINITY) continue;
+            double tmax = -INFINITY;
+            for (int i = p + lane; i < C; i += 32) tmax = fmax(tmax, x[i]);
+            tmax = warp_max(tmax);
+            double t2 = 0.0;
+            for (int i = p + lane; i < C; i += 32) t2 = __dadd_rn(t2, csvd_exp(__dsub_rn(x[i], tmax)));
+            t2 = warp_sum(t2);
+            if (lane == 0) o.lrh[p] = __dadd_rn(tmax, csvd_log(t2));
+        }
+        __syncthreads();
+    }
 }
 
 // cluster summary (warp): top-min(k,n) values desc, LSE, min, max of the
 // cluster's logits S_logits[lo, hi)
-__device__ __noinline__ void cluster_summary(const Dev &D, int lo, int hi, int k, double *topk, double *lse_o,
-                                             double *min_o, double *max_o, int lane) {
+#define SUM_E 8  // clusters of up to 32 * SUM_E rows are summarised from registers
+// logits of one cluster into registers (-inf padded); only for n <= 32 * SUM_E
+__device__ __forceinline__ void summary_load(const Dev &D, int lo, int hi, double (&reg)[SUM_E], int lane) {
+    const int n = hi - lo;
+#pragma unroll
+    for (int e = 0; e < SUM_E; ++e) {
+        const int i = lane + 32 * e;
+        reg[e] = (i < n && n <= 32 * SUM_E) ? __ldcg(D.S_logits + lo + i) : -INFINITY;
+    }
+}
+
+// reg: the cluster's logits from summary_load (ignored when n > 32 * SUM_E)
+static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int hi, int k, double *topk, double *lse_o,
+                                                       double *min_o, double *max_o, double (&reg)[SUM_E],
+                                                       int lane) {
     const int n = hi - lo;
     const double *v = D.S_logits + lo;
     const int kk = n < k ? n : k;
-    constexpr int E = 4;
-    double reg[E];
+    constexpr int E = SUM_E;
     const bool in_regs = n <= 32 * E;
     double mx = -INFINITY, mn = INFINITY;
     if (in_regs) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int i = lane + 32 * e;
-            reg[e] = i < n ? __ldcg(v + i) : -INFINITY;
-            if (i < n) {
+            if (lane + 32 * e < n) {
                 mx = fmax(mx, reg[e]);
                 mn = fmin(mn, reg[e]);
             }
@@ -444,8 +730,10 @@ __device__ __noinline__ void cluster_summary(const Dev &D, int lo, int hi, int k
             mn = fmin(mn, x);
         }
     }
+    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 48);
     mx = warp_max(mx);
     mn = warp_min(mn);
+    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 49);
     double s = 0.0;
     if (in_regs) {
 #pragma unroll
@@ -455,25 +743,49 @@ __device__ __noinline__ void cluster_summary(const Dev &D, int lo, int hi, int k
         for (int i = lane; i < n; i += 32) s = __dadd_rn(s, csvd_exp(__dsub_rn(__ldcg(v + i), mx)));
     }
     s = warp_sum(s);
-    // iterative selection in (value desc, index asc) order
-    double pv = INFINITY;
-    int pi = -1;
+    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 50);
+    if (in_regs) {
+        // top-kk values (only the values matter: the list holds no ids).
+        // Each lane sorts its 8 values (Batcher network), then kk rounds of a
+        // warp max over the lane heads with REDUX on the order-preserving
+        // 64-bit keys; the winning lane pops its head.
+#define CSVD_CAS(a, b)                  \
+    {                                   \
+        const double hi_ = fmax(reg[a], reg[b]); \
+        reg[b] = fmin(reg[a], reg[b]);  \
+        reg[a] = hi_;                   \
+    }
+        CSVD_CAS(0, 1) CSVD_CAS(2, 3) CSVD_CAS(4, 5) CSVD_CAS(6, 7)
+        CSVD_CAS(0, 2) CSVD_CAS(1, 3) CSVD_CAS(4, 6) CSVD_CAS(5, 7)
+        CSVD_CAS(1, 2) CSVD_CAS(5, 6) CSVD_CAS(0, 4) CSVD_CAS(3, 7)
+        CSVD_CAS(1, 5) CSVD_CAS(2, 6)
+        CSVD_CAS(1, 4) CSVD_CAS(3, 6)
+        CSVD_CAS(2, 4) CSVD_CAS(3, 5)
+        CSVD_CAS(3, 4)
+#undef CSVD_CAS
+    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 51);
 #pragma unroll 1
-    for (int j = 0; j < kk; ++j) {
-        double bv = -INFINITY;
-        int bi = 0x7fffffff;
-        if (in_regs) {
+        for (int j = 0; j < kk; ++j) {
+            const unsigned long long key = dkey(reg[0]);
+            const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+            const unsigned mh = __reduce_max_sync(CSVD_FULL, hi);
+            const unsigned ml = __reduce_max_sync(CSVD_FULL, hi == mh ? lo : 0u);
+            const unsigned win = __ballot_sync(CSVD_FULL, hi == mh && lo == ml);
+            if (lane == 0) topk[j] = dkey_inv(((unsigned long long)mh << 32) | ml);
+            if (lane == __ffs(win) - 1) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int i = lane + 32 * e;
-                const double x = reg[e];
-                const bool after = (x < pv) || (x == pv && i > pi);
-                if (i < n && after && (x > bv || (x == bv && i < bi))) {
-                    bv = x;
-                    bi = i;
-                }
+                for (int e = 0; e < E - 1; ++e) reg[e] = reg[e + 1];
+                reg[E - 1] = -INFINITY;
             }
-        } else {
+        }
+    } else {
+        // iterative selection in (value desc, index asc) order (clusters > 256 rows)
+        double pv = INFINITY;
+        int pi = -1;
+#pragma unroll 1
+        for (int j = 0; j < kk; ++j) {
+            double bv = -INFINITY;
+            int bi = 0x7fffffff;
             for (int i = lane; i < n; i += 32) {
                 const double x = __ldcg(v + i);
                 const bool after = (x < pv) || (x == pv && i > pi);
@@ -482,19 +794,19 @@ __device__ __noinline__ void cluster_summary(const Dev &D, int lo, int hi, int k
                     bi = i;
                 }
             }
-        }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(CSVD_FULL, bv, o);
-            const int oi = __shfl_xor_sync(CSVD_FULL, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-                bv = ov;
-                bi = oi;
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(CSVD_FULL, bv, o);
+                const int oi = __shfl_xor_sync(CSVD_FULL, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
             }
+            if (lane == 0) topk[j] = bv;
+            pv = bv;
+            pi = bi;
         }
-        if (lane == 0) topk[j] = bv;
-        pv = bv;
-        pi = bi;
     }
     if (lane == 0) {
         *lse_o = (mx == -INFINITY) ? -INFINITY : __dadd_rn(mx, csvd_log(s));
@@ -515,7 +827,7 @@ __device__ __forceinline__ double reg_merge(double v, double nv /* lane l: l-th 
 }
 
 // smem merge-path merge of two descending lists (k > 32 path)
-__device__ int merge_lists(const double *A, int ka, const double *B, int kb, int k, double *out, int lane) {
+static __device__ int merge_lists(const double *A, int ka, const double *B, int kb, int k, double *out, int lane) {
     for (int i = lane; i < ka; i += 32) {
         const double a = A[i];
         int lo = 0, hi = kb;  // count B > a
@@ -539,8 +851,19 @@ __device__ int merge_lists(const double *A, int ka, const double *B, int kb, int
     return n < k ? n : k;
 }
 
+// running top-16 list (k <= 16): lane l < 16 holds the l-th largest; lanes >= 16 hold -inf
+__device__ __forceinline__ double reg_merge16(double v, double nv /* lane l: l-th largest of new */, int lane) {
+    double m = fmax(v, __shfl_sync(CSVD_FULL, nv, 15 - (lane & 15)));  // bitonic: top-16 of the union
+#pragma unroll
+    for (int s = 8; s; s >>= 1) {
+        const double o = __shfl_xor_sync(CSVD_FULL, m, s);
+        m = ((lane & s) == 0) ? fmax(m, o) : fmin(m, o);
+    }
+    return lane < 16 ? m : -INFINITY;
+}
+
 // logsumexp over S_logits[0, n) with known max (64-merge recompute, certify.py:79-83)
-__device__ double warp_lse_all(const double *vals, int n, double vmax, int lane) {
+static __device__ double warp_lse_all(const double *vals, int n, double vmax, int lane) {
     if (n == 0 || vmax == -INFINITY) return -INFINITY;
     if (vmax == INFINITY) return INFINITY;
     double s = 0.0;
@@ -553,13 +876,13 @@ struct ScanShared {
     ScanState st;
     csvd_result res;
     int kcount;
-    int pad;
+    int head_n;  // > 0: the ordering is valid only for positions [0, head_n] (fast path)
 };
 
 // warp 0: per-prefix values of the chunk [q0, q1) from its summaries, then the
 // state machine (scan.cuh).  reg_list: the k <= 32 running list (lane-held);
 // la / lb: the k > 32 running list buffers (the live list stays in la).
-__device__ __noinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &ss, int q0, int q1,
+static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &ss, int q0, int q1,
                                         const double *c_topk, const double *c_lse, const double *c_min,
                                         const double *c_max, double *c_vals, double *la0, double *lb0,
                                         double &reg_list, int lane) {
@@ -585,25 +908,26 @@ __device__ __noinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &
         pmn = fmin(pmn, st0.smin);
         pmx = fmax(pmx, st0.smax);
     }
-    // streaming log Z_S: prefix-LSE of the cluster LSEs after the carry
-    double im = act ? lse_q : -INFINITY, is = act ? 1.0 : 0.0;
-#pragma unroll 1
-    for (int s = 1; s < 32; s <<= 1) {
-        const double m2 = __shfl_up_sync(CSVD_FULL, im, s), s2 = __shfl_up_sync(CSVD_FULL, is, s);
-        if (lane >= s) {
-            double mm = m2, sv = s2;
-            lse_combine(mm, sv, im, is);
-            im = mm;
-            is = sv;
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 40);
+    // streaming log Z_S (certify.py:83 logaddexp chain) as a prefix sum of
+    // exp(lse - M) over the chunk, M the chunk's largest term (incl. the carry)
+    double lz;
+    {
+        const double M = fmax(warp_max(act ? lse_q : -INFINITY), st0.log_z);
+        if (M == -INFINITY) {
+            lz = -INFINITY;
+        } else {
+            double t = (act && lse_q != -INFINITY) ? csvd_exp(__dsub_rn(lse_q, M)) : 0.0;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const double u = __shfl_up_sync(CSVD_FULL, t, s);
+                if (lane >= s) t = __dadd_rn(t, u);
+            }
+            if (st0.log_z != -INFINITY) t = __dadd_rn(t, csvd_exp(__dsub_rn(st0.log_z, M)));
+            lz = t > 0.0 ? __dadd_rn(M, csvd_log(t)) : -INFINITY;
         }
     }
-    {
-        double mm = st0.log_z, sv = (st0.log_z == -INFINITY) ? 0.0 : 1.0;
-        lse_combine(mm, sv, im, is);
-        im = mm;
-        is = sv;
-    }
-    double lz = (im == -INFINITY) ? -INFINITY : __dadd_rn(im, csvd_log(is));
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 41);
     // the reference recomputes log Z_S over all of S when the merge count p % 64 == 0
     const int rlane = (q0 / 64) * 64 + 63 - q0;
     if (rlane < q1 - q0) {
@@ -626,34 +950,50 @@ __device__ __noinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &
         if (lane == rlane) lz = full;
         if (lane > rlane) lz = (mm == -INFINITY) ? -INFINITY : __dadd_rn(mm, csvd_log(sv));
     }
-    // k-th largest after each merge (exact): sequential list merges
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 42);
+    // k-th largest after each merge (exact)
     double my_kth = -INFINITY;
     int kc = ss.kcount;
-    double *la = la0, *lb = lb0;
+    if (k <= 16) {
+        // sequential merges of 16-entry lists (lane l < 16 holds the l-th largest)
 #pragma unroll 1
-    for (int t = 0; t < q1 - q0; ++t) {
-        const int size = o.cum[q0 + t + 1] - o.cum[q0 + t];
-        const int kn = size < k ? size : k;
-        if (small_k) {
+        for (int t = 0; t < q1 - q0; ++t) {
+            const int size = o.cum[q0 + t + 1] - o.cum[q0 + t];
+            const int kn = size < k ? size : k;
             const double nv = lane < kn ? c_topk[t * k + lane] : -INFINITY;
-            reg_list = reg_merge(reg_list, nv, lane);
+            reg_list = reg_merge16(reg_list, nv, lane);
             kc = min(k, kc + kn);
             const double kv = __shfl_sync(CSVD_FULL, reg_list, k - 1);
             if (lane == t) my_kth = kc >= k ? kv : -INFINITY;
-        } else {
-            kc = merge_lists(la, kc, c_topk + t * k, kn, k, lb, lane);
-            double *tmp = la;
-            la = lb;
-            lb = tmp;
-            const double kv = kc >= k ? la[k - 1] : -INFINITY;
-            if (lane == t) my_kth = kv;
+        }
+    } else {  // k > 16
+        double *la = la0, *lb = lb0;
+#pragma unroll 1
+        for (int t = 0; t < q1 - q0; ++t) {
+            const int size = o.cum[q0 + t + 1] - o.cum[q0 + t];
+            const int kn = size < k ? size : k;
+            if (small_k) {
+                const double nv = lane < kn ? c_topk[t * k + lane] : -INFINITY;
+                reg_list = reg_merge(reg_list, nv, lane);
+                kc = min(k, kc + kn);
+                const double kv = __shfl_sync(CSVD_FULL, reg_list, k - 1);
+                if (lane == t) my_kth = kc >= k ? kv : -INFINITY;
+            } else {
+                kc = merge_lists(la, kc, c_topk + t * k, kn, k, lb, lane);
+                double *tmp = la;
+                la = lb;
+                lb = tmp;
+                const double kv = kc >= k ? la[k - 1] : -INFINITY;
+                if (lane == t) my_kth = kv;
+                __syncwarp();
+            }
+        }
+        if (!small_k && la != la0) {  // keep the live list in la0
+            for (int t = lane; t < kc; t += 32) la0[t] = la[t];
             __syncwarp();
         }
     }
-    if (!small_k && la != la0) {  // keep the live list in la0
-        for (int t = lane; t < kc; t += 32) la0[t] = la[t];
-        __syncwarp();
-    }
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 43);
     double *c_lz = c_vals, *c_kth = c_vals + CHUNK, *c_mn = c_vals + 2 * CHUNK, *c_mx = c_vals + 3 * CHUNK;
     double *c_rho = c_vals + 4 * CHUNK, *c_dl = c_vals + 5 * CHUNK;
     if (act) {
@@ -671,6 +1011,7 @@ __device__ __noinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &
     ScanState stl = st0;
     Scan sc{in, stl, res};
     const csvd_config &cfg = *D.cfg;
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 44);
     if (stl.phase == PH_MAIN && cfg.variant == CSVD_VARIANT_INCREMENTAL) {
         // Common path, all prefixes of the chunk at once: the first prefix that
         // trips the budget (decode.py:342) or passes a target (decode.py:192-210).
@@ -698,7 +1039,9 @@ __device__ __noinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &
             stl.heap_pops = stl.p;
         }
     }
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 45);
     sc.run(chk);
+    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 46);
     __syncwarp();
     if (lane == 0) {
         ss.st = stl;
@@ -786,7 +1129,7 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
 }
 
 // k-th largest over rows of `row_len` valid entries with stride `stride` (exact radix select)
-__device__ __noinline__ double block_kth_largest(const double *vals, int n, int row_len, int stride, int k) {
+static __device__ __forceinline__ double block_kth_largest(const double *vals, int n, int row_len, int stride, int k) {
     __shared__ unsigned hist[256];
     __shared__ unsigned long long s_pref;
     __shared__ int s_k;
@@ -825,7 +1168,10 @@ __device__ __noinline__ double block_kth_largest(const double *vals, int n, int 
 }
 
 // scan state at p = 0 and the first wave (thread 0; shared-memory searches)
-__device__ __noinline__ void init_state(const Dev &D, const Ord &o, ScanShared &ss) {
+// head_n > 0: only positions [0, head_n] of the ordering exist yet (order_head);
+// the first wave is the head, and the budget cap is computed once the full
+// order exists (the kernel builds it before planning past the head).
+static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, ScanShared &ss, int head_n) {
     const csvd_config &cfg = *D.cfg;
     ScanState st;
     memset(&st, 0, sizeof(st));
@@ -838,24 +1184,39 @@ __device__ __noinline__ void init_state(const Dev &D, const Ord &o, ScanShared &
     st.delta = INFINITY;
     ScanIn in{D.cfg, D.C, (long long)D.V, D.d, o.cum, o.Uo, o.lrh};
     ScalarSearch search;
-    st.p_sel = (cfg.variant == CSVD_VARIANT_BATCHSELECT) ? csvd_select_prefix(in, cfg.k_max, search) : 0;
-    st.p_cap = csvd_cap_prefix(in, st.p_sel, search);
+    if (head_n == 0) {
+        st.p_sel = (cfg.variant == CSVD_VARIANT_BATCHSELECT) ? csvd_select_prefix(in, cfg.k_max, search) : 0;
+        st.p_cap = csvd_cap_prefix(in, st.p_sel, search);
+    } else {
+        st.p_sel = 0;
+        st.p_cap = D.C;
+    }
     const long long wt = cfg.first_wave_tokens > 0 ? cfg.first_wave_tokens : 1;
     st.wave_tokens = (int)min(wt, (long long)D.V);
     const int c0 = o.order[0];
     st.est = (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? __ldcg(D.dots + c0)
                                                   : __dadd_rn(__ldcg(D.dots + c0), D.meanb[c0]);
     st.p_lo = 0;
-    st.p_hi = csvd_plan_wave(st, in, search);
+    st.p_hi = head_n > 0 ? head_n : csvd_plan_wave(st, in, search);
     st.mode = MODE_SPARSE;
     st.wave_tokens = st.wave_tokens * 2 < D.V ? st.wave_tokens * 2 : (int)D.V;
     ss.st = st;
     memset(&ss.res, 0, sizeof(ss.res));
     ss.kcount = 0;
+    ss.head_n = head_n;
 }
 
-// after a wave's scan: done / dense / next wave (thread 0)
-__device__ __noinline__ void next_wave(const Dev &D, const Ord &o, ScanShared &ss) {
+// fast path eligibility: the head is the first wave of an incremental step
+// with a top-k target under the default wave policy
+__device__ __forceinline__ bool head_eligible(const csvd_config &cfg) {
+    if (cfg.variant != CSVD_VARIANT_INCREMENTAL || cfg.first_wave_tokens > 0) return false;
+    for (int t = 0; t < cfg.n_targets; ++t)
+        if (cfg.targets[t] == CSVD_TARGET_TOPK) return true;
+    return false;
+}
+
+// after a wave's scan: done / dense / next wave (thread 0): done / dense / next wave (thread 0)
+static __device__ __forceinline__ void next_wave(const Dev &D, const Ord &o, ScanShared &ss) {
     ScanState s2 = ss.st;
     s2.iter += 1;
     if (s2.phase == PH_DONE) {
@@ -892,12 +1253,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
     double *scratch = smem + D.scratch_off + warp * (CSVD_MAX_LEAVES / 4);
     double *ws = smem + D.ord_off;
     double *sws = smem + D.sum_off;
-    __shared__ RankShared rs;
     __shared__ ScanShared ss;
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
     if (lead) DBG_TS(D, 0);
     if (D.launch_mode != LAUNCH_BOUNDS) pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
     if (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b) pw_stage<BCPL>(D.bplan, D.h, D.d, hs_b, D.bsrc);
+    if (D.launch_mode != LAUNCH_DENSE && lane == 0) {
+        // start the HBM reads of this warp's centroid rows (and, in CTA 0, the
+        // per-cluster arrays every CTA reads later) while h is staged
+        const int c = warp * gridDim.x + blockIdx.x;
+        if (c < D.C) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
+        if (blockIdx.x == 0 && warp == WARPS - 1) {
+            bulk_prefetch_l2(D.logsz, sizeof(double) * D.C);
+            bulk_prefetch_l2(D.sizes, sizeof(int) * D.C);
+            bulk_prefetch_l2(D.meanb, sizeof(double) * D.C);
+            bulk_prefetch_l2(D.radii, sizeof(double) * D.C);
+            bulk_prefetch_l2(D.maxb, sizeof(double) * D.C);
+            bulk_prefetch_l2(D.starts, sizeof(int) * D.C);
+        }
+    }
     if (threadIdx.x == 0) {
         memset(&ss, 0, sizeof(ss));
         if (D.launch_mode == LAUNCH_DENSE) {
@@ -920,17 +1294,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
         if (lead) DBG_TS(D, 2);
         grid_sync(D);
         if (lead) DBG_TS(D, 3);
-        const bool ok = rank_phase(D, ws, rs);
-        if (lead) DBG_TS(D, 4);
+        const bool ok = stage_bounds(D, o);
         if (!ok || D.launch_mode == LAUNCH_BOUNDS) {
-            grid_sync(D);  // final U visible before the host reads it
             if (lead) D.res->error = ok ? 0 : CSVD_EVALUE;
             return;
         }
-        grid_sync(D);
+        const int hn = head_eligible(*D.cfg) ? order_head(D, o) : 0;
+        if (lead && D.dbg) D.dbg[63] = (unsigned long long)hn;
         if (lead) DBG_TS(D, 5);
-        load_ordering(D, o);
-        if (threadIdx.x == 0) init_state(D, o, ss);
+        if (hn == 0) order_full(D, o);
+        if (lead) DBG_TS(D, 4);
+        if (threadIdx.x == 0) init_state(D, o, ss, hn);
         __syncthreads();
         if (lead) DBG_TS(D, 6);
     }
@@ -949,16 +1323,41 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             // summaries + scan, chunk by chunk (identical in every CTA)
             for (int q0 = st.p_lo; q0 < st.p_hi; q0 += D.chunk) {
                 const int q1 = min(st.p_hi, q0 + D.chunk);
-                for (int q = q0 + warp; q < q1; q += WARPS)
-                    cluster_summary(D, o.cum[q], o.cum[q + 1], k, c_topk + (q - q0) * k, c_lse + (q - q0),
-                                    c_min + (q - q0), c_max + (q - q0), lane);
+                {  // the loads of this warp's next two clusters are always in flight
+                    double pre[2][SUM_E];
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int q = q0 + warp + t * WARPS;
+                        if (q < q1) summary_load(D, o.cum[q], o.cum[q + 1], pre[t], lane);
+                    }
+#pragma unroll 1
+                    for (int q = q0 + warp; q < q1; q += WARPS) {  // one copy of the summary code
+                        cluster_summary(D, o.cum[q], o.cum[q + 1], k, c_topk + (q - q0) * k, c_lse + (q - q0),
+                                        c_min + (q - q0), c_max + (q - q0), pre[0], lane);
+#pragma unroll
+                        for (int e = 0; e < SUM_E; ++e) pre[0][e] = pre[1][e];
+                        const int qn = q + 2 * WARPS;
+                        if (qn < q1) summary_load(D, o.cum[qn], o.cum[qn + 1], pre[1], lane);
+                    }
+                }
                 __syncthreads();
                 if (lead) DBG_TS(D, 10 + 4 * (st.iter & 3));
                 if (warp == 0) scan_chunk(D, o, ss, q0, q1, c_topk, c_lse, c_min, c_max, c_vals, la, lb, reg_list, lane);
                 __syncthreads();
                 if (ss.st.phase != PH_MAIN && ss.st.phase != PH_PE) break;
             }
+            if (ss.head_n > 0 && (ss.st.phase == PH_MAIN || ss.st.phase == PH_PE)) {
+                // the head is exhausted: build the full order, then plan as usual
+                order_full(D, o);
+                if (threadIdx.x == 0) {
+                    ScanIn in{D.cfg, D.C, (long long)D.V, D.d, o.cum, o.Uo, o.lrh};
+                    ss.st.p_cap = csvd_cap_prefix(in, ss.st.p_sel, ScalarSearch{});
+                    ss.head_n = 0;
+                }
+                __syncthreads();
+            }
             if (threadIdx.x == 0) next_wave(D, o, ss);
+            if (lead) DBG_TS(D, 47);
             __syncthreads();
             if (lead) DBG_TS(D, 11 + 4 * (st.iter & 3));
         } else {  // MODE_DENSE

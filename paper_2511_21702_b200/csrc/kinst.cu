@@ -1,0 +1,9 @@
+// Explicit instantiations of the step kernel, one weight dtype / row plan per
+// translation unit (compiled in parallel by build.py with -DKI_ET, -DKI_CPL,
+// -DKI_Q); csvd_b200.cu declares them `extern template`.
+#include "kernels.cuh"
+
+#if KI_CPL > 0
+template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q>(Dev);
+#endif
+template __global__ void k_step<KI_ET, KI_CPL, KI_Q, 0, 0>(Dev);

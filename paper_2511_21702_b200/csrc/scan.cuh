@@ -59,10 +59,10 @@ struct ScanState {
 };
 
 #ifdef __CUDACC__
-__device__ __noinline__ double csvd_ddiv(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __noinline__ double csvd_exp(double x) { return exp(x); }
-__device__ __noinline__ double csvd_log(double x) { return log(x); }
-__device__ __noinline__ double csvd_log1p(double x) { return log1p(x); }
+static __device__ __noinline__ double csvd_ddiv(double a, double b) { return __ddiv_rn(a, b); }
+static __device__ __noinline__ double csvd_exp(double x) { return exp(x); }
+static __device__ __noinline__ double csvd_log(double x) { return log(x); }
+static __device__ __noinline__ double csvd_log1p(double x) { return log1p(x); }
 #endif
 #ifdef __CUDA_ARCH__
 #define CSVD_ADD(a, b) __dadd_rn((a), (b))

@@ -19,10 +19,14 @@ lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
 names = {0: "kernel start", 1: "h staged", 2: "cta0 bounds done", 3: "barrier1 passed",
-         4: "rank done (cta0)", 5: "barrier2 passed", 6: "ordering loaded + planned"}
+         4: "order done (head|full)", 5: "head done", 6: "wave 1 planned", 30: "  U loaded", 31: "  sorted",
+         32: "  cum/x done", 33: "  e done", 34: "  lrh done", 35: "  lrh done (RESCALE)",
+         40: "  scan: min/max", 41: "  scan: lse prefix", 42: "  scan: 64-merge", 43: "  scan: kth lists",
+         44: "  scan: rho/delta", 45: "  scan: ballot/jump", 46: "  scan: run", 47: "  next_wave",
+         48: "  sum: loaded", 49: "  sum: min/max", 50: "  sum: exp-sum", 51: "  sum: sorted", 52: "  sum: loads issued", 53: "  sum: loads landed"}
 for w in range(4):
     names.update({8 + 4 * w: f"wave{w} rows start", 9 + 4 * w: f"wave{w} barrier passed",
-                  10 + 4 * w: f"wave{w} summaries done", 11 + 4 * w: f"wave{w} scan+plan done"})
+                  10 + 4 * w: f"wave{w} summaries loaded", 11 + 4 * w: f"wave{w} scan+plan done"})
 for i, h in enumerate(q):
     buf = np.zeros(128, dtype=np.uint64)
     import ctypes as C_
@@ -33,6 +37,8 @@ for i, h in enumerate(q):
     if i < 2:
         continue
     t0 = int(buf[0])
+    print(f"head n = {int(buf[63])}")
+    buf[63] = 0
     print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} fb={out.fallback_used}")
     prev = None
     for slot in sorted(names, key=lambda s: int(buf[s]) if buf[s] else 1 << 62):
