@@ -103,7 +103,29 @@ typedef struct {
     int32_t variant;                  /* CSVD_VARIANT_* */
     int32_t slack_f32;                /* cfg.slack_mode == "f32" (bounds.py:58-64) */
     int64_t first_wave_tokens;        /* speculative wave policy; 0 = default */
+    int32_t shard_lo, shard_hi;       /* csvd_shard_open: opening positions [lo, hi); hi 0 = the
+                                         batch-select prefix (decode.py:346-359) */
 } csvd_config;
+
+/* Per-shard aggregate of one csvd_shard_open call (sharded_decode_step,
+ * shard_sim.py:134-208): everything a rank contributes to the merge, plus the
+ * global-order facts every rank computes identically.  Layout of the double
+ * buffer returned by csvd_shard_open / csvd_shard_dense: */
+#define CSVD_SH_LSE 0        /* log-sum-exp of this shard's logits in the range      */
+#define CSVD_SH_MIN 1        /* min / max of them (+inf / -inf when none)             */
+#define CSVD_SH_MAX 2
+#define CSVD_SH_NTOK 3       /* tokens of this shard in the range                     */
+#define CSVD_SH_NLIST 4      /* entries in the top-k list (min(k, NTOK))              */
+#define CSVD_SH_P_LO 5       /* resolved range [p_lo, p_hi) in opening positions      */
+#define CSVD_SH_P_HI 6
+#define CSVD_SH_P_SEL 7      /* batch-select prefix                                   */
+#define CSVD_SH_CUM_LO 8     /* tokens before p_lo / p_hi in the global opening order */
+#define CSVD_SH_CUM_HI 9
+#define CSVD_SH_U_NEXT 10    /* bound at position p_hi (max unopened), -inf if p_hi == C */
+#define CSVD_SH_LRH_NEXT 11  /* log R-hat after opening [0, p_hi)                     */
+#define CSVD_SH_QNORM 12
+#define CSVD_SH_SLACK 13
+#define CSVD_SH_TOPK 16      /* then the shard's top-k logits (descending)            */
 
 /* CertStatus + StepMetrics scalars (certify.py:48-53, decode.py:118-130). */
 typedef struct {
@@ -132,6 +154,26 @@ int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *table,
                 const csvd_index_desc *index);
 int csvd_destroy(csvd_ctx *ctx);
 const char *csvd_strerror(csvd_ctx *ctx);
+
+/* Shard context for vocabulary-sharded decoding (shard_sim.py:84-208 made
+ * real): every cluster's centroid / bound data is replicated (bounds and the
+ * opening order are computed identically on every rank), but only the W rows
+ * of clusters with owned[c] != 0 are uploaded and ever read. */
+int csvd_create_shard(csvd_ctx **out, int device, const csvd_table_desc *table,
+                      const csvd_index_desc *index, const uint8_t *owned);
+
+/* Open the owned clusters among opening positions [cfg->shard_lo, hi) (hi =
+ * cfg->shard_hi, or the batch-select prefix when 0) from HOST h: bounds and the
+ * global order on the device, this shard's rows, its aggregate (CSVD_SH_*,
+ * `summary` holds CSVD_SH_TOPK + k doubles), and its tokens in the range in
+ * opening order: global opening position, token id, logit (n_out entries). */
+int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config *cfg, double *summary,
+                    int64_t *positions, int64_t *ids, double *logits, int64_t cap, int64_t *n_out);
+
+/* Full-vocabulary fallback on this shard (decode.py:239-262): logits of the
+ * owned tokens (ids ascending) and the shard's top-k list in `summary`. */
+int csvd_shard_dense(csvd_ctx *ctx, const double *h, int32_t k, double *summary, int64_t *ids,
+                     double *logits, int64_t cap, int64_t *n_out);
 
 /* Workspace capacity for k (top-k list length); grows on demand. */
 int csvd_reserve_k(csvd_ctx *ctx, int32_t k);

@@ -68,6 +68,8 @@ class Config(ctypes.Structure):
         ("variant", ctypes.c_int32),
         ("slack_f32", ctypes.c_int32),
         ("first_wave_tokens", ctypes.c_int64),
+        ("shard_lo", ctypes.c_int32),
+        ("shard_hi", ctypes.c_int32),
     ]
 
 
@@ -95,7 +97,7 @@ EXPORTS = (
     "csvd_create", "csvd_destroy", "csvd_strerror", "csvd_reserve_k", "csvd_step_host",
     "csvd_step_device", "csvd_outputs", "csvd_bounds_host", "csvd_dense_host",
     "csvd_dense_device", "csvd_info", "csvd_last_launches", "csvd_stream", "csvd_set_direct",
-    "csvd_l2_flush",
+    "csvd_l2_flush", "csvd_create_shard", "csvd_shard_open", "csvd_shard_dense",
 )
 
 _lib = None
@@ -122,6 +124,9 @@ def load():
     P = ctypes.c_void_p
     vp = ctypes.POINTER(ctypes.c_void_p)
     lib.csvd_create.argtypes = [vp, ctypes.c_int, ctypes.POINTER(TableDesc), ctypes.POINTER(IndexDesc)]
+    lib.csvd_create_shard.argtypes = [vp, ctypes.c_int, ctypes.POINTER(TableDesc), ctypes.POINTER(IndexDesc), P]
+    lib.csvd_shard_open.argtypes = [P, P, ctypes.POINTER(Config), P, P, P, P, ctypes.c_int64, P]
+    lib.csvd_shard_dense.argtypes = [P, P, ctypes.c_int32, P, P, P, ctypes.c_int64, P]
     lib.csvd_destroy.argtypes = [P]
     lib.csvd_strerror.argtypes = [P]
     lib.csvd_strerror.restype = ctypes.c_char_p

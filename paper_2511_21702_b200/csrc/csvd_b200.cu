@@ -5,6 +5,7 @@
 // full-vocabulary fallback) is decided on the device inside k_step.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -69,6 +70,13 @@ struct csvd_ctx {
     int64_t first_chunk = 0;
     std::vector<int2> wleaves, bleaves;
     std::vector<short> wprog, bprog;
+    // shard contexts
+    bool shard = false;
+    std::vector<uint8_t> owned;      // [C]
+    std::vector<int> order_h, cum_h;  // staging for csvd_shard_open
+    std::vector<long long> sids_h;
+    std::vector<double> slog_h, sum_h;
+    std::vector<long long> local_tokens;  // owned token ids, ascending
 };
 
 static int fail(csvd_ctx *c, int code, const std::string &msg) {
@@ -220,6 +228,9 @@ static int alloc_k(csvd_ctx *ctx, int K) {
     CK(cudaMalloc(&p, sizeof(double) * (size_t)D.C * K + 16));
     ctx->k_buffers[1] = p;
     D.sum_topk = (double *)p;
+    CK(cudaMalloc(&p, sizeof(double) * (CSVD_SH_TOPK + (size_t)K) + 16));
+    ctx->k_buffers[2] = p;
+    D.shard_out = (double *)p;
     D.K = K;
     return 0;
 }
@@ -300,7 +311,8 @@ extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
     return build_graphs(ctx);
 }
 
-extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t, const csvd_index_desc *ix) {
+static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, const csvd_index_desc *ix,
+                       const uint8_t *owned) {
     if (!out || !t || !ix) return CSVD_ECONFIG;
     csvd_ctx *ctx = new csvd_ctx();
     *out = ctx;
@@ -358,21 +370,58 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     const long long V = D.V;
     const size_t esz = (D.wdtype == CSVD_W_BF16) ? 2 : 4;
     const size_t row_bytes = esz * (size_t)D.d;
+    // local rows: every row (unsharded) or the owned clusters' rows, cluster by
+    // cluster in id order (each cluster stays one contiguous row range)
+    const int Cn = ix->n_clusters;
+    ctx->shard = owned != nullptr;
+    ctx->owned.assign(Cn, 1);
+    if (owned)
+        for (int c = 0; c < Cn; ++c) ctx->owned[c] = owned[c] ? 1 : 0;
+    std::vector<int> wrow0(Cn, -1), lpos;
+    std::vector<long long> lperm;  // local row -> original token id
+    {
+        int lr = 0;
+        for (int c = 0; c < Cn; ++c) {
+            if (!ctx->owned[c]) continue;
+            wrow0[c] = lr;
+            for (long long i = 0; i < ix->sizes[c]; ++i) {
+                const long long pos = ix->starts[c] + i;
+                if (pos < 0 || pos >= V) return fail(ctx, CSVD_ECONFIG, "cluster ranges out of range");
+                lpos.push_back((int)pos);
+                lperm.push_back(ix->perm[pos]);
+                ++lr;
+            }
+        }
+        D.Vl = lr;
+    }
+    ctx->local_tokens.assign(lperm.begin(), lperm.end());
+    std::sort(ctx->local_tokens.begin(), ctx->local_tokens.end());
     if (t->weights) {
         void *Wtmp = nullptr, *W = nullptr;
         CK(cudaMalloc(&Wtmp, row_bytes * V));
         CK(cudaMemcpy(Wtmp, t->weights, row_bytes * V, cudaMemcpyHostToDevice));
         long long *dperm64;
-        if ((rc = dupload(ctx, &dperm64, (const long long *)ix->perm, (size_t)V))) return rc;
-        CK(cudaMalloc(&W, row_bytes * V + 64));
+        if ((rc = dupload(ctx, &dperm64, lperm.data(), lperm.size()))) return rc;
+        CK(cudaMalloc(&W, row_bytes * (size_t)(D.Vl > 0 ? D.Vl : 1) + 64));
         ctx->dev_allocs.push_back(W);
-        k_permute_rows<<<4096, 256>>>((const char *)Wtmp, (char *)W, dperm64, V, (long long)row_bytes);
+        if (D.Vl > 0)
+            k_permute_rows<<<4096, 256>>>((const char *)Wtmp, (char *)W, dperm64, D.Vl, (long long)row_bytes);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         CK(cudaFree(Wtmp));
         D.W = W;
     } else {
         D.W = nullptr;
+    }
+    {
+        int *dw;
+        if ((rc = dupload(ctx, &dw, wrow0.data(), wrow0.size()))) return rc;
+        D.wrow0 = dw;
+        D.lpos = nullptr;
+        if (owned) {
+            if ((rc = dupload(ctx, &dw, lpos.data(), lpos.size() ? lpos.size() : 1))) return rc;
+            D.lpos = dw;
+        }
     }
     std::vector<float> biasp(V);
     std::vector<int> perm32(V);
@@ -441,6 +490,8 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     if ((rc = dalloc(ctx, &D.Uraw, C))) return rc;
     if ((rc = dalloc(ctx, &D.cnt, C))) return rc;
     CK(cudaMemset(D.cnt, 0, sizeof(int) * C));
+    if ((rc = dalloc(ctx, &D.order_g, C))) return rc;
+    if ((rc = dalloc(ctx, &D.cum_g, C + 1))) return rc;
     if ((rc = dalloc(ctx, &D.sum_lse, C))) return rc;
     if ((rc = dalloc(ctx, &D.sum_min, C))) return rc;
     if ((rc = dalloc(ctx, &D.sum_max, C))) return rc;
@@ -471,6 +522,16 @@ extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t,
     if ((rc = alloc_k(ctx, 32))) return rc;
     if ((rc = configure(ctx))) return rc;
     return build_graphs(ctx);
+}
+
+extern "C" int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *t, const csvd_index_desc *ix) {
+    return create_impl(out, device, t, ix, nullptr);
+}
+
+extern "C" int csvd_create_shard(csvd_ctx **out, int device, const csvd_table_desc *t, const csvd_index_desc *ix,
+                                 const uint8_t *owned) {
+    if (!owned) return CSVD_ECONFIG;
+    return create_impl(out, device, t, ix, owned);
 }
 
 extern "C" int csvd_destroy(csvd_ctx *ctx) {
@@ -649,6 +710,98 @@ extern "C" int csvd_dense_device(csvd_ctx *ctx, const double *h_dev, void *strea
     if (h_dev && h_dev != ctx->d_h)
         CK(cudaMemcpyAsync(ctx->d_h, h_dev, sizeof(double) * ctx->D.d, cudaMemcpyDeviceToDevice, s));
     return dense_async(ctx, s);
+}
+
+// ---------------------------------------------------------------------------
+// shard entry points (sharded_decode_step, shard_sim.py:134-208)
+// ---------------------------------------------------------------------------
+extern "C" int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config *cfg, double *summary,
+                               int64_t *positions, int64_t *ids, double *logits, int64_t cap, int64_t *n_out) {
+    if (!ctx || !h || !cfg || !summary || !n_out) return CSVD_ESTATE;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    int rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    if (cfg->variant != CSVD_VARIANT_BATCHSELECT) return fail(ctx, CSVD_ECONFIG, "shard opens use batch-select order");
+    const Dev &D = ctx->D;
+    memcpy(ctx->h_pin, h, sizeof(double) * D.d);
+    *ctx->cfg_pin = *cfg;
+    CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * D.d, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    if ((rc = launch(ctx, LAUNCH_SHARD, s))) return rc;
+    const int K = D.K;
+    ctx->sum_h.resize(CSVD_SH_TOPK + K);
+    ctx->order_h.resize(D.C);
+    ctx->cum_h.resize(D.C + 1);
+    CK(cudaMemcpyAsync(ctx->res_pin, D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->sum_h.data(), D.shard_out, sizeof(double) * (CSVD_SH_TOPK + K), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->order_h.data(), D.order_g, sizeof(int) * D.C, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->cum_h.data(), D.cum_g, sizeof(int) * (D.C + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((rc = result_error(ctx, *ctx->res_pin))) return rc;
+    const double *sm = ctx->sum_h.data();
+    const int p_lo = (int)sm[CSVD_SH_P_LO], p_hi = (int)sm[CSVD_SH_P_HI];
+    const long long c_lo = ctx->cum_h[p_lo], c_hi = ctx->cum_h[p_hi];
+    const long long nrange = c_hi - c_lo;
+    // this shard's tokens of the range, in opening order
+    long long n = 0;
+    for (int q = p_lo; q < p_hi; ++q)
+        if (ctx->owned[ctx->order_h[q]]) n += ctx->cum_h[q + 1] - ctx->cum_h[q];
+    *n_out = n;
+    memcpy(summary, sm, sizeof(double) * (CSVD_SH_TOPK + cfg->k));
+    if (n > cap) return fail(ctx, CSVD_EDIM, "output capacity too small");
+    if (n == 0 || (!positions && !ids && !logits)) return 0;
+    ctx->sids_h.resize(nrange);
+    ctx->slog_h.resize(nrange);
+    CK(cudaMemcpyAsync(ctx->sids_h.data(), D.S_ids + c_lo, sizeof(long long) * nrange, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->slog_h.data(), D.S_logits + c_lo, sizeof(double) * nrange, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    long long j = 0;
+    for (int q = p_lo; q < p_hi; ++q) {
+        if (!ctx->owned[ctx->order_h[q]]) continue;
+        for (long long r = ctx->cum_h[q]; r < ctx->cum_h[q + 1]; ++r, ++j) {
+            if (positions) positions[j] = r;
+            if (ids) ids[j] = ctx->sids_h[r - c_lo];
+            if (logits) logits[j] = ctx->slog_h[r - c_lo];
+        }
+    }
+    return 0;
+}
+
+extern "C" int csvd_shard_dense(csvd_ctx *ctx, const double *h, int32_t k, double *summary, int64_t *ids,
+                                double *logits, int64_t cap, int64_t *n_out) {
+    if (!ctx || !h || !summary || !n_out) return CSVD_ESTATE;
+    if (!ctx->shard) return fail(ctx, CSVD_ECONFIG, "not a shard context");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const Dev &D0 = ctx->D;
+    if (k < 1 || k > D0.V) return fail(ctx, CSVD_ECONFIG, "need 1 <= k <= V");
+    int rc;
+    if (k > D0.K && (rc = csvd_reserve_k(ctx, k))) return rc;
+    const Dev &D = ctx->D;
+    fixed_cfg(ctx->cfg_pin, D.V, 0);
+    ctx->cfg_pin->k = k;
+    memcpy(ctx->h_pin, h, sizeof(double) * D.d);
+    CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * D.d, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    if ((rc = launch(ctx, LAUNCH_DENSE, s))) return rc;
+    ctx->sum_h.resize(CSVD_SH_TOPK + D.K);
+    CK(cudaMemcpyAsync(ctx->res_pin, D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->sum_h.data(), D.shard_out, sizeof(double) * (CSVD_SH_TOPK + D.K), cudaMemcpyDeviceToHost, s));
+    const long long V = D.V;
+    CK(cudaMemcpyAsync(ctx->logits_pin, D.S_logits, sizeof(double) * V, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((rc = result_error(ctx, *ctx->res_pin))) return rc;
+    const long long n = (long long)ctx->local_tokens.size();
+    *n_out = n;
+    memcpy(summary, ctx->sum_h.data(), sizeof(double) * (CSVD_SH_TOPK + k));
+    if (n > cap) return fail(ctx, CSVD_EDIM, "output capacity too small");
+    for (long long j = 0; j < n; ++j) {
+        const long long tok = ctx->local_tokens[j];
+        if (ids) ids[j] = tok;
+        if (logits) logits[j] = ctx->logits_pin[tok];
+    }
+    return 0;
 }
 
 extern "C" int csvd_info(csvd_ctx *ctx, int64_t *V, int64_t *d, int32_t *C, int32_t *bd, int32_t *wreg, int32_t *breg,

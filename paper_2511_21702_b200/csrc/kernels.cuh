@@ -42,7 +42,7 @@
 #define MAX_PER_WARP 8  // clusters per warp in the bounds / rank phases
 #define CHUNK 32        // max clusters per scan chunk (one per lane)
 
-enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2 };
+enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2, LAUNCH_SHARD = 3 };
 
 struct Dev {
     int V, d, C, Cp, bd, mode, wdtype;  // Cp: C rounded up to a power of two (sort)
@@ -53,6 +53,14 @@ struct Dev {
     const double *cent; // [C, bd]
     const double *radii, *maxb, *cnorm, *ang, *maxn, *minn, *logsz, *meanb;
     const int *starts, *sizes;
+    // W rows present on this device: cluster c's rows start at local row
+    // wrow0[c] (-1: another shard owns c); dense walks local rows lr < Vl,
+    // global position lpos[lr] (lpos null: lr itself, the unsharded table)
+    const int *wrow0;
+    const int *lpos;
+    int Vl;
+    int *order_g, *cum_g;    // shard opens: the opening order / prefix counts for the host
+    double *shard_out;       // CSVD_SH_* aggregate (K + CSVD_SH_TOPK doubles)
     PwPlan wplan, bplan;
     const int *wsrc, *bsrc;  // interleaved-layout source tables (CPL < 8 plans)
     // per step
@@ -197,8 +205,9 @@ static __device__ __forceinline__ void grid_sync(const Dev &D) {
 }
 
 template <typename ET, int CPL, int Q>
-__device__ __forceinline__ double row_logit(const Dev &D, int pos, const double *hs, double *scratch, int lane) {
-    const ET *row = reinterpret_cast<const ET *>(D.W) + (size_t)pos * D.d;
+__device__ __forceinline__ double row_logit(const Dev &D, int wrow, int pos, const double *hs, double *scratch,
+                                            int lane) {
+    const ET *row = reinterpret_cast<const ET *>(D.W) + (size_t)wrow * D.d;
     double dot = warp_dot_t<ET, CPL, Q>(row, hs, D.wplan, scratch, lane);
     return __dadd_rn(dot, (double)__ldg(D.bias + pos));
 }
@@ -1067,8 +1076,9 @@ __device__ void wave_rows(const Dev &D, const Ord &o, int p_lo, int p_hi, const 
                 const int mid = (lo + hi) >> 1;
                 if (o.cum[mid] <= r) lo = mid; else hi = mid;
             }
-            const int pos = D.starts[o.order[lo]] + (r - o.cum[lo]);
-            bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)pos * rb, rb);
+            const int w0 = D.wrow0[o.order[lo]];
+            if (w0 >= 0)
+                bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(w0 + r - o.cum[lo]) * rb, rb);
         }
     }
     for (int r = row_lo + gwarp; r < row_hi; r += nwarps) {
@@ -1077,8 +1087,12 @@ __device__ void wave_rows(const Dev &D, const Ord &o, int p_lo, int p_hi, const 
             const int mid = (lo + hi) >> 1;
             if (o.cum[mid] <= r) lo = mid; else hi = mid;
         }
-        const int pos = D.starts[o.order[lo]] + (r - o.cum[lo]);
-        const double logit = row_logit<ET, CPL, Q>(D, pos, hs, scratch, lane);
+        const int c = o.order[lo];
+        const int w0 = D.wrow0[c];
+        if (w0 < 0) continue;  // another shard's cluster
+        const int i = r - o.cum[lo];
+        const int pos = D.starts[c] + i;
+        const double logit = row_logit<ET, CPL, Q>(D, w0 + i, pos, hs, scratch, lane);
         if (lane == 0) {
             D.S_logits[r] = logit;
             D.S_ids[r] = (long long)__ldg(D.perm + pos);
@@ -1099,8 +1113,9 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
     double lv = -INFINITY;  // small k: lane l holds the l-th largest so far
     int cnt = 0;
     double kmin = -INFINITY;
-    for (int pos = gwarp; pos < D.V; pos += nwarps) {
-        const double logit = row_logit<ET, CPL, Q>(D, pos, hs, scratch, lane);
+    for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
+        const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
+        const double logit = row_logit<ET, CPL, Q>(D, lr, pos, hs, scratch, lane);
         if (lane == 0) {
             const int tok = __ldg(D.perm + pos);
             D.S_logits[tok] = logit;
@@ -1242,6 +1257,115 @@ static __device__ __forceinline__ void next_wave(const Dev &D, const Ord &o, Sca
 }
 
 // ---------------------------------------------------------------------------
+// shard open (LAUNCH_SHARD): this shard's part of sharded_decode_step
+// (shard_sim.py:134-208).  The global order is already in shared memory (every
+// rank computes it identically from the replicated bounds); the shard computes
+// the rows of its clusters among positions [p_lo, p_hi) and CTA 0 reduces them
+// to the merge record: LSE, min, max, token count and top-k list.
+// ---------------------------------------------------------------------------
+template <typename ET, int CPL, int Q>
+__device__ void shard_open(const Dev &D, const Ord &o, ScanShared &ss, const double *hs, double *scratch,
+                           double *sws) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const csvd_config &cfg = *D.cfg;
+    const int C = D.C, k = cfg.k;
+    const int p_lo = min(max(cfg.shard_lo, 0), C);
+    const int p_hi = max(p_lo, min(cfg.shard_hi > 0 ? cfg.shard_hi : ss.st.p_sel, C));
+    wave_rows<ET, CPL, Q>(D, o, p_lo, p_hi, hs, scratch);
+    grid_sync(D);
+    if (blockIdx.x != 0) return;
+    double *c_lse = sws, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
+    double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
+    __shared__ int s_own[CHUNK];
+    double reg_list = -INFINITY, m = -INFINITY, ssum = 0.0, mn = INFINITY, mx = -INFINITY;
+    int kc = 0, ntok = 0;
+    for (int q0 = p_lo; q0 < p_hi; q0 += D.chunk) {
+        const int q1 = min(p_hi, q0 + D.chunk);
+        for (int q = q0 + warp; q < q1; q += WARPS) {
+            const bool own = D.wrow0[o.order[q]] >= 0;
+            if (lane == 0) s_own[q - q0] = own;
+            if (own) {
+                double pre[SUM_E];
+                summary_load(D, o.cum[q], o.cum[q + 1], pre, lane);
+                cluster_summary(D, o.cum[q], o.cum[q + 1], k, c_topk + (q - q0) * k, c_lse + (q - q0),
+                                c_min + (q - q0), c_max + (q - q0), pre, lane);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+#pragma unroll 1
+            for (int t = 0; t < q1 - q0; ++t) {
+                if (!s_own[t]) continue;
+                const int size = o.cum[q0 + t + 1] - o.cum[q0 + t];
+                const int kn = size < k ? size : k;
+                ntok += size;
+                lse_combine(m, ssum, c_lse[t], 1.0);
+                mn = fmin(mn, c_min[t]);
+                mx = fmax(mx, c_max[t]);
+                if (k <= 32) {
+                    const double nv = lane < kn ? c_topk[t * k + lane] : -INFINITY;
+                    reg_list = reg_merge(reg_list, nv, lane);
+                    kc = min(k, kc + kn);
+                } else {
+                    kc = merge_lists(la, kc, c_topk + t * k, kn, k, lb, lane);
+                    for (int j = lane; j < kc; j += 32) la[j] = lb[j];
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double *out = D.shard_out;
+    if (warp == 0) {
+        if (k <= 32) {
+            if (lane < kc) out[CSVD_SH_TOPK + lane] = reg_list;
+        } else {
+            for (int j = lane; j < kc; j += 32) out[CSVD_SH_TOPK + j] = la[j];
+        }
+        if (lane == 0) {
+            out[CSVD_SH_LSE] = (m == -INFINITY) ? -INFINITY : __dadd_rn(m, csvd_log(ssum));
+            out[CSVD_SH_MIN] = mn;
+            out[CSVD_SH_MAX] = mx;
+            out[CSVD_SH_NTOK] = (double)ntok;
+            out[CSVD_SH_NLIST] = (double)kc;
+            out[CSVD_SH_P_LO] = (double)p_lo;
+            out[CSVD_SH_P_HI] = (double)p_hi;
+            out[CSVD_SH_P_SEL] = (double)ss.st.p_sel;
+            out[CSVD_SH_CUM_LO] = (double)o.cum[p_lo];
+            out[CSVD_SH_CUM_HI] = (double)o.cum[p_hi];
+            out[CSVD_SH_U_NEXT] = p_hi < C ? o.Uo[p_hi] : -INFINITY;
+            out[CSVD_SH_LRH_NEXT] = o.lrh[p_hi];
+            out[CSVD_SH_QNORM] = D.res->query_norm;
+            out[CSVD_SH_SLACK] = D.res->slack;
+        }
+    }
+    for (int q = tid; q <= C; q += THREADS) {
+        if (q < C) D.order_g[q] = o.order[q];
+        D.cum_g[q] = o.cum[q];
+    }
+}
+
+// dense on a shard: the shard's top-k list (values above its k-th largest,
+// then copies of the k-th) for the cross-shard merge; CTA 0
+static __device__ void shard_dense_list(const Dev &D, double kth, int k) {
+    __shared__ int s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int n = D.nblocks * WARPS * k;
+    for (int i = threadIdx.x; i < n; i += THREADS) {
+        const double v = __ldcg(D.cand + (size_t)(i / k) * D.K + (i % k));
+        if (v > kth) D.shard_out[CSVD_SH_TOPK + atomicAdd(&s_cnt, 1)] = v;
+    }
+    __syncthreads();
+    const int nl = min(k, D.Vl);
+    for (int j = s_cnt + threadIdx.x; j < nl; j += THREADS) D.shard_out[CSVD_SH_TOPK + j] = kth;
+    if (threadIdx.x == 0) {
+        D.shard_out[CSVD_SH_NTOK] = (double)D.Vl;
+        D.shard_out[CSVD_SH_NLIST] = (double)nl;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // the step kernel
 // ---------------------------------------------------------------------------
 template <typename ET, int CPL, int Q, int BCPL, int BQ>
@@ -1307,6 +1431,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
         if (threadIdx.x == 0) init_state(D, o, ss, hn);
         __syncthreads();
         if (lead) DBG_TS(D, 6);
+        if (D.launch_mode == LAUNCH_SHARD) {
+            shard_open<ET, CPL, Q>(D, o, ss, hs_w, scratch, sws);
+            return;
+        }
     }
     // chunk scratch: [6*CHUNK values][CHUNK lse][CHUNK min][CHUNK max][2 K-lists][chunk*k topk]
     double *c_vals = sws, *c_lse = sws + 6 * CHUNK, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
@@ -1365,6 +1493,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             grid_sync(D);
             if (blockIdx.x != 0) break;
             const double kth = block_kth_largest(D.cand, D.nblocks * WARPS * k, k, D.K, k);
+            if (D.lpos) shard_dense_list(D, kth, k);
             if (threadIdx.x == 0) {
                 ScanIn in{D.cfg, D.C, (long long)D.V, D.d, nullptr, nullptr, nullptr};
                 csvd_result r;

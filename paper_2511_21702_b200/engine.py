@@ -66,7 +66,7 @@ class DeviceIndex:
     """
 
     def __init__(self, table, index, device: int = 0, check_fingerprint: bool = True,
-                 weights_required: bool = True):
+                 weights_required: bool = True, owned=None):
         lib = _lib.load()
         if table is not None and check_fingerprint:
             if index.fingerprint != table_fingerprint(table):
@@ -130,7 +130,12 @@ class DeviceIndex:
             ix.max_norms = c(index.max_norms, np.float64).ctypes.data
             ix.min_norms = c(index.min_norms, np.float64).ctypes.data
         self._ctx = ctypes.c_void_p()
-        rc = lib.csvd_create(ctypes.byref(self._ctx), device, ctypes.byref(td), ctypes.byref(ix))
+        if owned is None:
+            rc = lib.csvd_create(ctypes.byref(self._ctx), device, ctypes.byref(td), ctypes.byref(ix))
+        else:  # vocabulary shard: only the owned clusters' W rows are uploaded
+            own = c(owned, np.uint8)
+            rc = lib.csvd_create_shard(ctypes.byref(self._ctx), device, ctypes.byref(td), ctypes.byref(ix),
+                                       own.ctypes.data)
         if rc != 0:
             msg = lib.csvd_strerror(self._ctx).decode()
             lib.csvd_destroy(self._ctx)

@@ -229,17 +229,42 @@ def ledger_for(index, plan: ShardPlan, outcome, latency: LatencyModel = LatencyM
                       omega_comm=(tb + tl) / total if total > 0 else 0.0)
 
 
-def sharded_decode_step(table, index, plan: ShardPlan, h, cfg, k_max=None, latency: LatencyModel = LatencyModel()):
-    """B200 `csvd.sharded_decode_step` (shard_sim.py:134-208) in one process.
+_DECODERS: dict = {}
 
-    The outcome is the batch-select step (bit-identical for every N and
-    strategy, which is the reference's contract); the ledger is the
-    reference's accounting."""
+
+def _distributed_world():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_world_size()
+    except Exception:  # pragma: no cover
+        pass
+    return 1
+
+
+def sharded_decode_step(table, index, plan: ShardPlan, h, cfg, k_max=None, latency: LatencyModel = LatencyModel()):
+    """B200 `csvd.sharded_decode_step` (shard_sim.py:134-208).
+
+    Inside a torch.distributed process group whose size equals
+    plan.n_workers, every rank is one worker: it owns the plan's clusters on
+    its GPU and the step runs as `distributed.ShardedDecoder` (one all_gather
+    of per-shard merge records).  Otherwise (one process) the N workers are
+    simulated as in the reference: the outcome is the batch-select step,
+    bit-identical for every N and strategy by construction.  Either way the
+    ledger is the reference's accounting."""
     validate_config(cfg, index.vocab_size)
     if np.asarray(plan.assignment).shape != (index.n_clusters,):
         raise ValueError("plan does not cover this index")
     k_max = resolved_k_max(cfg, index.vocab_size) if k_max is None else k_max
-    outcome = engine.decode_step_batchselect(table, index, h, cfg, k_max=k_max)
+    if plan.n_workers > 1 and _distributed_world() == plan.n_workers:
+        from .distributed import ShardedDecoder
+        key = (id(table), id(index), id(plan))
+        dec = _DECODERS.get(key)
+        if dec is None:
+            dec = _DECODERS[key] = ShardedDecoder(table, index, plan)
+        outcome = dec.step(h, cfg, k_max=k_max)
+    else:
+        outcome = engine.decode_step_batchselect(table, index, h, cfg, k_max=k_max)
     return outcome, ledger_for(index, plan, outcome, latency)
 
 

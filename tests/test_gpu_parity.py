@@ -117,3 +117,26 @@ def test_errors_mirror_reference():
     bad.fingerprint = b"x" * 32
     with pytest.raises(P.ConfigError):
         P.decode_step(T, bad, h, P.DecodeConfig())
+
+
+def test_head_fast_path_and_general_path_agree():
+    """The kernel orders clusters two ways: the head fast path (only clusters
+    whose bound beats the best-logit estimate, sorted by one warp) and the full
+    block sort.  first_wave_tokens > 0 forces the full sort.  Both must equal
+    the oracle, including steps where the head is exhausted (partial expand
+    past it, tight budgets) and where it is too large (random queries)."""
+    from paper_2511_21702_b200 import _lib
+    T, ix = _c1_like(V=32000, d=4096, n_modes=64, g=4)
+    q = np.vstack([wl.generate_queries(4, 4096, "contextual", 7, centroids=ix.centroids),
+                   wl.generate_queries(2, 4096, "random", 8)])
+    ctx = P.prepare(T, ix)
+    cfgs = [P.DecodeConfig(k=10), P.DecodeConfig(k=10, k_max=300), P.DecodeConfig(k=3, k_max=150),
+            P.DecodeConfig(k=16)]
+    for ci, cfg in enumerate(cfgs):
+        for i, h in enumerate(q):
+            e = _fields(O.decode_step(T, ix, h, cfg))
+            for fwt in (0, 1):
+                c = ctx.make_config(cfg, first_wave_tokens=fwt)
+                assert c.variant == _lib.VARIANT_INCREMENTAL
+                got = ctx.step(h, c)
+                assert_outcome(got, e, rtol=TRANS_RTOL, where=f"head[{ci},{i},fwt={fwt}]")
