@@ -175,6 +175,19 @@ int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config *cfg, doub
 int csvd_shard_dense(csvd_ctx *ctx, const double *h, int32_t k, double *summary, int64_t *ids,
                      double *logits, int64_t cap, int64_t *n_out);
 
+/* Batched decode: B independent decode_step calls (decode.py:312-343) in one
+ * graph replay.  Each query runs the step kernel on its own slice of the GPU
+ * (a cooperative grid of ~148/B CTAs; all B run concurrently, sharing the
+ * centroid and W reads through L2).  H: [B, d] host doubles; res[B];
+ * ids / logits: B rows of `cap` entries (query b's |S| entries at row b). */
+int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, const csvd_config *cfg,
+                         csvd_result *res, int64_t *ids, double *logits, int64_t cap);
+/* Device-resident variant (H_dev: [B, d] device doubles), asynchronous. */
+int csvd_step_batch_device(csvd_ctx *ctx, int32_t B, const double *H_dev, const csvd_config *cfg,
+                           void *stream);
+/* Lanes currently built and the CTAs each lane's step runs on. */
+int csvd_batch_lanes(csvd_ctx *ctx, int32_t *lanes, int32_t *grid_per_lane);
+
 /* Workspace capacity for k (top-k list length); grows on demand. */
 int csvd_reserve_k(csvd_ctx *ctx, int32_t k);
 

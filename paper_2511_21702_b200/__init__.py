@@ -31,6 +31,7 @@ from .engine import (
     clear_cache,
     cluster_bounds,
     decode_step,
+    decode_step_batch,
     decode_step_batchselect,
     dense_logits,
     prepare,
@@ -43,6 +44,6 @@ __all__ = [
     "BoundVector", "CertStatus", "ClusterIndex", "ClusterMeta", "ConfigError", "DecodeConfig",
     "DecodeOutcome", "DenseResult", "EmbeddingTable", "FingerprintMismatchError", "FullVocab",
     "PartialExpand", "RelaxEps", "StepMetrics", "DeviceIndex", "clear_cache", "cluster_bounds",
-    "decode_step", "decode_step_batchselect", "dense_logits", "prepare", "CommLedger",
+    "decode_step", "decode_step_batch", "decode_step_batchselect", "dense_logits", "prepare", "CommLedger",
     "LatencyModel", "ShardPlan", "make_plan", "sharded_decode_step",
 ]

@@ -98,6 +98,7 @@ EXPORTS = (
     "csvd_step_device", "csvd_outputs", "csvd_bounds_host", "csvd_dense_host",
     "csvd_dense_device", "csvd_info", "csvd_last_launches", "csvd_stream", "csvd_set_direct",
     "csvd_l2_flush", "csvd_create_shard", "csvd_shard_open", "csvd_shard_dense",
+    "csvd_step_batch_host", "csvd_step_batch_device", "csvd_batch_lanes",
 )
 
 _lib = None
@@ -127,6 +128,9 @@ def load():
     lib.csvd_create_shard.argtypes = [vp, ctypes.c_int, ctypes.POINTER(TableDesc), ctypes.POINTER(IndexDesc), P]
     lib.csvd_shard_open.argtypes = [P, P, ctypes.POINTER(Config), P, P, P, P, ctypes.c_int64, P]
     lib.csvd_shard_dense.argtypes = [P, P, ctypes.c_int32, P, P, P, ctypes.c_int64, P]
+    lib.csvd_step_batch_host.argtypes = [P, ctypes.c_int32, P, ctypes.POINTER(Config), P, P, P, ctypes.c_int64]
+    lib.csvd_step_batch_device.argtypes = [P, ctypes.c_int32, P, ctypes.POINTER(Config), P]
+    lib.csvd_batch_lanes.argtypes = [P, P, P]
     lib.csvd_destroy.argtypes = [P]
     lib.csvd_strerror.argtypes = [P]
     lib.csvd_strerror.restype = ctypes.c_char_p

@@ -46,6 +46,16 @@ __global__ void k_l2_flush(const uint4 *buf, size_t n, unsigned *sink) {
 // ---------------------------------------------------------------------------
 typedef void (*kern_t)(Dev);
 
+// A batch lane: one query's step running on its own slice of the GPU (a
+// cooperative grid of ~148/B CTAs) concurrently with the other lanes.  Lanes
+// share every read-only table / index buffer (W rows and centroids are read
+// through the shared L2) and own their per-step workspaces.
+struct Lane {
+    Dev D{};
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+};
+
 struct csvd_ctx {
     int device = 0;
     Dev D{};
@@ -77,6 +87,19 @@ struct csvd_ctx {
     std::vector<long long> sids_h;
     std::vector<double> slog_h, sum_h;
     std::vector<long long> local_tokens;  // owned token ids, ascending
+    // batch lanes (decode_step over a batch of queries)
+    std::vector<Lane> lanes;
+    std::vector<void *> lane_allocs;
+    int lane_grid = 0, lane_K = 0;
+    double *d_H = nullptr;                 // [lanes, d]
+    csvd_result *d_res_all = nullptr;      // [lanes]
+    double *H_pin = nullptr;
+    csvd_result *res_pin_b = nullptr;
+    long long *ids_pin_b = nullptr;
+    double *logits_pin_b = nullptr;
+    cudaEvent_t fork = nullptr;
+    cudaGraphExec_t g_batch = nullptr;
+    int g_batch_B = 0, g_batch_host = 0;
 };
 
 static int fail(csvd_ctx *c, int code, const std::string &msg) {
@@ -298,6 +321,201 @@ static int build_graphs(csvd_ctx *ctx) {
     return 0;
 }
 
+static int check_cfg(csvd_ctx *ctx, const csvd_config *cfg);
+
+static void free_lanes(csvd_ctx *ctx) {
+    if (ctx->g_batch) cudaGraphExecDestroy(ctx->g_batch);
+    ctx->g_batch = nullptr;
+    ctx->g_batch_B = 0;
+    for (Lane &l : ctx->lanes) {
+        if (l.stream) cudaStreamDestroy(l.stream);
+        if (l.done) cudaEventDestroy(l.done);
+    }
+    ctx->lanes.clear();
+    for (void *p : ctx->lane_allocs) cudaFree(p);
+    ctx->lane_allocs.clear();
+    if (ctx->H_pin) cudaFreeHost(ctx->H_pin);
+    if (ctx->res_pin_b) cudaFreeHost(ctx->res_pin_b);
+    if (ctx->ids_pin_b) cudaFreeHost(ctx->ids_pin_b);
+    if (ctx->logits_pin_b) cudaFreeHost(ctx->logits_pin_b);
+    ctx->H_pin = nullptr;
+    ctx->res_pin_b = nullptr;
+    ctx->ids_pin_b = nullptr;
+    ctx->logits_pin_b = nullptr;
+    ctx->lane_grid = 0;
+}
+
+template <typename T>
+static int lalloc(csvd_ctx *ctx, T **p, size_t count) {
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+    if (e != cudaSuccess) return fail(ctx, CSVD_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    ctx->lane_allocs.push_back(q);
+    *p = reinterpret_cast<T *>(q);
+    return 0;
+}
+
+// B lanes, each a full per-step workspace and a grid of max(1, grid / B) CTAs
+static int ensure_lanes(csvd_ctx *ctx, int B) {
+    const Dev &D0 = ctx->D;
+    const int G = ctx->grid / B > 0 ? ctx->grid / B : 1;
+    if ((int)ctx->lanes.size() == B && ctx->lane_grid == G && ctx->lane_K == D0.K) return 0;
+    free_lanes(ctx);
+    const int C = D0.C, V = D0.V, K = D0.K;
+    if ((long long)C > (long long)MAX_PER_WARP * G * WARPS)
+        return fail(ctx, CSVD_ECONFIG, "too many clusters for a batch lane's grid (use a smaller batch)");
+    int rc;
+    if ((rc = lalloc(ctx, &ctx->d_H, (size_t)B * D0.d))) return rc;
+    if ((rc = lalloc(ctx, &ctx->d_res_all, (size_t)B))) return rc;
+    CK(cudaMemset(ctx->d_res_all, 0, sizeof(csvd_result) * B));
+    const int first = (int)ctx->first_chunk;
+    CK(cudaHostAlloc(&ctx->H_pin, sizeof(double) * B * D0.d, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->res_pin_b, sizeof(csvd_result) * B, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->ids_pin_b, sizeof(long long) * B * first, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->logits_pin_b, sizeof(double) * B * first, cudaHostAllocDefault));
+    ctx->lanes.resize(B);
+    for (int b = 0; b < B; ++b) {
+        Lane &l = ctx->lanes[b];
+        Dev L = D0;  // shared read-only table / index data, own workspaces
+        L.h = ctx->d_H + (size_t)b * D0.d;
+        L.res = ctx->d_res_all + b;
+        if ((rc = lalloc(ctx, &L.U, C)) || (rc = lalloc(ctx, &L.Uraw, C)) || (rc = lalloc(ctx, &L.dots, C)) ||
+            (rc = lalloc(ctx, &L.cnt, C)) || (rc = lalloc(ctx, &L.order_g, C)) ||
+            (rc = lalloc(ctx, &L.cum_g, C + 1)) || (rc = lalloc(ctx, &L.sum_lse, C)) ||
+            (rc = lalloc(ctx, &L.sum_min, C)) || (rc = lalloc(ctx, &L.sum_max, C)) ||
+            (rc = lalloc(ctx, &L.S_logits, (size_t)V)) || (rc = lalloc(ctx, &L.S_ids, (size_t)V)) ||
+            (rc = lalloc(ctx, &L.st, 1)) || (rc = lalloc(ctx, &L.bar, 4)) ||
+            (rc = lalloc(ctx, &L.cand, (size_t)G * WARPS * K)) || (rc = lalloc(ctx, &L.sum_topk, (size_t)C * K)) ||
+            (rc = lalloc(ctx, &L.shard_out, (size_t)CSVD_SH_TOPK + K)))
+            return rc;
+        CK(cudaMemset(L.cnt, 0, sizeof(int) * C));
+        CK(cudaMemset(L.bar, 0, 16));
+        CK(cudaMemset(L.st, 0, sizeof(ScanState)));
+        L.nblocks = G;
+        L.dbg = nullptr;
+        l.D = L;
+        CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+    }
+    if (!ctx->fork) CK(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    ctx->lane_grid = G;
+    ctx->lane_K = K;
+    return 0;
+}
+
+// the batch graph: [H2D H, cfg] -> fork -> B lane kernels -> join [-> D2H results + first chunks]
+static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
+    if (ctx->g_batch) cudaGraphExecDestroy(ctx->g_batch);
+    ctx->g_batch = nullptr;
+    cudaStream_t s = ctx->stream;
+    cudaGraph_t g;
+    const Dev &D0 = ctx->D;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    if (host_io)
+        CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->fork, s));
+    for (int b = 0; b < B; ++b) {
+        Lane &l = ctx->lanes[b];
+        CK(cudaStreamWaitEvent(l.stream, ctx->fork, 0));
+        Dev Dl = l.D;
+        Dl.launch_mode = LAUNCH_STEP;
+        void *args[] = {&Dl};
+        CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->lane_grid), dim3(THREADS), args, ctx->smem,
+                                       l.stream));
+        if (host_io) {
+            const int64_t first = ctx->first_chunk;
+            CK(cudaMemcpyAsync(ctx->ids_pin_b + (size_t)b * first, Dl.S_ids, sizeof(long long) * first,
+                               cudaMemcpyDeviceToHost, l.stream));
+            CK(cudaMemcpyAsync(ctx->logits_pin_b + (size_t)b * first, Dl.S_logits, sizeof(double) * first,
+                               cudaMemcpyDeviceToHost, l.stream));
+        }
+        CK(cudaEventRecord(l.done, l.stream));
+        CK(cudaStreamWaitEvent(s, l.done, 0));
+    }
+    if (host_io)
+        CK(cudaMemcpyAsync(ctx->res_pin_b, ctx->d_res_all, sizeof(csvd_result) * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamEndCapture(s, &g));
+    CK(cudaGraphInstantiate(&ctx->g_batch, g, 0));
+    CK(cudaGraphDestroy(g));
+    ctx->g_batch_B = B;
+    ctx->g_batch_host = host_io ? 1 : 0;
+    return 0;
+}
+
+static int batch_prepare(csvd_ctx *ctx, int B, const csvd_config *cfg, bool host_io) {
+    if (B < 1 || B > 1024) return fail(ctx, CSVD_ECONFIG, "batch size must be in [1, 1024]");
+    int rc = check_cfg(ctx, cfg);
+    if (rc) return rc;
+    if ((rc = ensure_lanes(ctx, B))) return rc;
+    *ctx->cfg_pin = *cfg;
+    if (!ctx->g_batch || ctx->g_batch_B != B || ctx->g_batch_host != (host_io ? 1 : 0))
+        if ((rc = capture_batch(ctx, B, host_io))) return rc;
+    return 0;
+}
+
+extern "C" int csvd_step_batch_device(csvd_ctx *ctx, int32_t B, const double *H_dev, const csvd_config *cfg,
+                                      void *stream) {
+    if (!ctx || !cfg || !H_dev) return CSVD_ESTATE;
+    CK(cudaSetDevice(ctx->device));
+    int rc = batch_prepare(ctx, B, cfg, false);
+    if (rc) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+    if (H_dev != ctx->d_H)
+        CK(cudaMemcpyAsync(ctx->d_H, H_dev, sizeof(double) * B * ctx->D.d, cudaMemcpyDeviceToDevice, s));
+    CK(cudaGraphLaunch(ctx->g_batch, s));
+    return 0;
+}
+
+extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, const csvd_config *cfg,
+                                    csvd_result *res, int64_t *ids, double *logits, int64_t cap) {
+    if (!ctx || !cfg || !H || !res) return CSVD_ESTATE;
+    CK(cudaSetDevice(ctx->device));
+    int rc = batch_prepare(ctx, B, cfg, true);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    memcpy(ctx->H_pin, H, sizeof(double) * B * ctx->D.d);
+    CK(cudaGraphLaunch(ctx->g_batch, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t first = ctx->first_chunk;
+    int err = 0;
+    for (int b = 0; b < B; ++b) {
+        res[b] = ctx->res_pin_b[b];
+        if (res[b].error && !err) err = b + 1;
+    }
+    if (err) {
+        CK(cudaMemset(ctx->d_res_all, 0, sizeof(csvd_result) * B));
+        for (Lane &l : ctx->lanes) {
+            CK(cudaMemset(l.D.bar, 0, 16));
+            CK(cudaMemset(l.D.cnt, 0, sizeof(int) * ctx->D.C));
+        }
+        const int e = res[err - 1].error;
+        return fail(ctx, e, e == CSVD_EVALUE ? "bounds must be finite" : "device state error (grid barrier timeout)");
+    }
+    for (int b = 0; b < B; ++b) {
+        const int64_t n = res[b].sub_size;
+        if (n > cap) return fail(ctx, CSVD_EDIM, "output capacity too small");
+        int64_t *ib = ids ? ids + (size_t)b * cap : nullptr;
+        double *lb = logits ? logits + (size_t)b * cap : nullptr;
+        const int64_t m = n < first ? n : first;
+        if (ib) memcpy(ib, ctx->ids_pin_b + (size_t)b * first, sizeof(int64_t) * m);
+        if (lb) memcpy(lb, ctx->logits_pin_b + (size_t)b * first, sizeof(double) * m);
+        if (n > first) {
+            const Dev &L = ctx->lanes[b].D;
+            if (ib) CK(cudaMemcpy(ib + first, L.S_ids + first, sizeof(int64_t) * (n - first), cudaMemcpyDeviceToHost));
+            if (lb) CK(cudaMemcpy(lb + first, L.S_logits + first, sizeof(double) * (n - first), cudaMemcpyDeviceToHost));
+        }
+    }
+    return 0;
+}
+
+extern "C" int csvd_batch_lanes(csvd_ctx *ctx, int32_t *lanes, int32_t *grid_per_lane) {
+    if (!ctx) return CSVD_ESTATE;
+    if (lanes) *lanes = (int32_t)ctx->lanes.size();
+    if (grid_per_lane) *grid_per_lane = ctx->lane_grid;
+    return 0;
+}
+
 extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
     if (!ctx) return CSVD_ESTATE;
     if (k <= ctx->D.K) return 0;
@@ -306,6 +524,7 @@ extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
     int rc;
+    free_lanes(ctx);  // lanes are rebuilt for the new K on the next batch
     if ((rc = alloc_k(ctx, K))) return rc;
     if ((rc = configure(ctx))) return rc;
     return build_graphs(ctx);
@@ -540,6 +759,8 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (cudaGraphExec_t g : {ctx->g_step, ctx->g_host, ctx->g_bounds, ctx->g_dense})
         if (g) cudaGraphExecDestroy(g);
+    free_lanes(ctx);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     for (void *p : ctx->dev_allocs) cudaFree(p);
     for (int i = 0; i < 4; ++i)
         if (ctx->k_buffers[i]) cudaFree(ctx->k_buffers[i]);

@@ -39,7 +39,7 @@
 #ifndef CSVD_SPIN_NS
 #define CSVD_SPIN_NS 64
 #endif
-#define MAX_PER_WARP 8  // clusters per warp in the bounds / rank phases
+#define MAX_PER_WARP 64  // clusters per warp in the bounds phase (small grids: batch lanes)
 #define CHUNK 32        // max clusters per scan chunk (one per lane)
 
 enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2, LAUNCH_SHARD = 3 };

@@ -190,6 +190,26 @@ class DeviceIndex:
             logits = self._logits[:n].copy()
         return self._outcome(r, ids, logits)
 
+    def step_batch(self, H, cfg, k_max=None, variant=_lib.VARIANT_INCREMENTAL) -> list:
+        """B queries in one graph replay (csvd_step_batch_host): outcome b equals
+        the single-query step on H[b]."""
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        if H.ndim != 2 or H.shape[1] != self.d:
+            raise ValueError(f"queries must have shape (B, {self.d})")
+        B = H.shape[0]
+        c = cfg if isinstance(cfg, _lib.Config) else self.make_config(cfg, k_max, variant)
+        res = (_lib.Result * B)()
+        ids = np.empty((B, self.V), dtype=np.int64)
+        logits = np.empty((B, self.V), dtype=np.float64)
+        with self._lock:
+            self._check(self._lib.csvd_step_batch_host(self._ctx, B, H.ctypes.data, ctypes.byref(c), res,
+                                                       ids.ctypes.data, logits.ctypes.data, self.V))
+        out = []
+        for b in range(B):
+            n = int(res[b].sub_size)
+            out.append(self._outcome(res[b], ids[b, :n].copy(), logits[b, :n].copy()))
+        return out
+
     def _outcome(self, r, ids, logits) -> DecodeOutcome:
         kind = _lib.KIND_NAMES.get(r.kind)
         if kind is None:
@@ -310,6 +330,14 @@ def decode_step(table, index, h, cfg, k_max=None) -> DecodeOutcome:
     """B200 `csvd.decode_step` (decode.py:312-343)."""
     ctx = prepare(table, index)
     return ctx.step(h, ctx.make_config(cfg, k_max, _lib.VARIANT_INCREMENTAL))
+
+
+def decode_step_batch(table, index, H, cfg, k_max=None) -> list:
+    """Batched decode: [decode_step(table, index, h, cfg, k_max) for h in H]
+    (the reference has no batched API), all B queries in
+    one graph replay on concurrent slices of the GPU."""
+    ctx = prepare(table, index)
+    return ctx.step_batch(H, ctx.make_config(cfg, k_max, _lib.VARIANT_INCREMENTAL))
 
 
 def decode_step_batchselect(table, index, h, cfg, k_max=None) -> DecodeOutcome:
