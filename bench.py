@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--first-wave-tokens", type=int, default=0)
     ap.add_argument("--direct", action="store_true", help="launch kernels without the CUDA graph (profiling)")
+    ap.add_argument("--no-batch", action="store_true", help="skip the batched (c3) measurement")
+    ap.add_argument("--batch-steps", type=int, default=40)
+    ap.add_argument("--sharded-steps", type=int, default=20)
     return ap.parse_args()
 
 
@@ -180,6 +183,102 @@ def cpu_baseline(T, ix, q, cfg, seconds):
             "fallback_rate": fb / max(n, 1)}
 
 
+C3 = dict(V=151552, d=3584, C=2273, g=1, dtype="bf16", B=16, eps=1e-3)
+
+
+def run_batched(a, torch, P, lib, ctypes):
+    """configs[2] (c3): Qwen2.5 head V=151552 d=3584 bf16, C=2273, batch 16,
+    epsilon-certified softmax eps=1e-3.  One graph replay decodes the whole
+    batch (B concurrent step lanes + shared batched bounds)."""
+    from paper_2511_21702_b200 import workload as wl
+    c = C3
+    T = wl.synth_vocab(c["V"], c["d"], c["C"] // c["g"], a.spread, 1, dtype=c["dtype"])
+    ix = wl.fast_index(T, c["C"] // c["g"], c["g"])
+    B, K = c["B"], a.batch_steps
+    Q = wl.generate_queries(B * (K + 3), c["d"], "contextual", 7, centroids=ix.centroids, noise=a.noise)
+    cfg = P.DecodeConfig(k=a.k, epsilon=c["eps"], targets=("softmax_eps",))
+    ctx = P.prepare(T, ix)
+    ccfg = ctx.make_config(cfg)
+    sp = ctypes.c_void_p()
+    lib.csvd_stream(ctx._ctx, ctypes.byref(sp))
+    ext = torch.cuda.ExternalStream(sp.value)
+    Hd = torch.from_numpy(Q).cuda()
+    # e2e through the public API: host queries in, host outcomes out
+    for i in range(3):
+        P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
+    e2e_t, outs = [], []
+    for i in range(3, K + 3):
+        lib.csvd_l2_flush(ctx._ctx, sp)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        o = P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
+        e2e_t.append(time.perf_counter() - t0)
+        outs += o
+    dev_ms = []
+    for i in range(K + 3):
+        lib.csvd_l2_flush(ctx._ctx, sp)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        rc = lib.csvd_step_batch_device(ctx._ctx, B, Hd[i * B:(i + 1) * B].data_ptr(), ctypes.byref(ccfg), sp)
+        e1.record(ext)
+        if rc != 0:
+            raise RuntimeError(lib.csvd_strerror(ctx._ctx).decode())
+        torch.cuda.synchronize()
+        if i >= 3:
+            dev_ms.append(e0.elapsed_time(e1))
+    ms = float(np.mean(dev_ms))
+    d, Cn = c["d"], ix.n_clusters
+    # algorithmic bytes per batch (SURVEY §8d, batched): centroids once, the
+    # B queries, the union of opened rows (bf16 + f32 bias), ids + logits out
+    union_rows = 0
+    for j in range(K):
+        grp = outs[j * B:(j + 1) * B]
+        union_rows += len(set().union(*[set(o.token_ids.tolist()) for o in grp]))
+    union_rows /= K
+    sub = float(np.mean([o.stats.sub_size for o in outs]))
+    bytes_b = 8 * Cn * d + 24 * Cn + B * 8 * d + union_rows * (2 * d + 4) + B * 12 * sub
+    pk, _ = peaks()
+    return {
+        "workload": f"qwen2.5-head V={c['V']} d={d} C={Cn} bf16 B={B} softmax_eps eps={c['eps']}",
+        "value": B * 1e3 / ms, "unit": "query-steps/s", "ms_per_batch": ms,
+        "e2e": {"value": B * K / sum(e2e_t), "unit": "query-steps/s",
+                "h2d_bytes_per_step": B * 8 * d + 152, "d2h_bytes_per_step": float(B * 88 + 16 * B * sub)},
+        "roofline": {"bound": "hbm", "achieved": bytes_b / (ms * 1e-3) / 1e9, "peak": pk, "unit": "GB/s",
+                     "frac": bytes_b / (ms * 1e-3) / 1e9 / pk, "algorithmic_bytes_per_batch": bytes_b},
+        "mean_sub_size": sub, "mean_clusters_opened": float(np.mean([o.stats.clusters_opened for o in outs])),
+        "fallback_rate": float(np.mean([o.fallback_used is not None for o in outs])),
+        "design": "B concurrent step lanes (cooperative grids of 148/B CTAs) after one shared batched-bounds kernel",
+    }
+
+
+def run_sharded(a, torch, P, dist, world, rank, T, ix, q):
+    """Vocabulary-sharded step (sharded_decode_step semantics) over the process
+    group: each rank owns a contiguous slab of clusters / W rows; one
+    all_gather of per-shard merge records per open."""
+    from paper_2511_21702_b200 import distributed as Dm, shard
+    plan = shard.contiguous_plan(ix, world)
+    dec = Dm.ShardedDecoder(T, ix, plan)
+    cfg = P.DecodeConfig(k=a.k)
+    for i in range(3):
+        dec.step(q[i], cfg)
+    K = a.sharded_steps
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    outs = [dec.step(q[3 + i], cfg) for i in range(K)]
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    sub = float(np.mean([o.stats.sub_size for o in outs]))
+    return {"semantics": "sharded_decode_step (batch-select, k_max = V/2)", "n_ranks": world,
+            "plan": "contiguous token-balanced", "steps_per_s": K / dt, "ms_per_step": 1e3 * dt / K,
+            "timing": "host wall clock around K steps, max over ranks (collectives sync every step)",
+            "mean_sub_size": sub, "comm_bytes_per_step_per_rank": dec.comm.bytes / (K + 3),
+            "fallback_rate": float(np.mean([o.fallback_used is not None for o in outs]))}
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -230,12 +329,13 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; more ranks than GPUs (gloo smoke runs on one B200) share devices
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     engine.DEFAULT_DEVICE = local
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("CSVD_DIST_BACKEND", "nccl"))
     T, ix, q = make_workload(a)
     cfg = P.DecodeConfig(k=a.k)
     ctx = P.prepare(T, ix)
@@ -306,10 +406,14 @@ def run_ours(a):
         if i >= 3:
             dense_ms.append(s0.elapsed_time(s1))
 
+    sharded = None
+    if world > 1:
+        sharded = run_sharded(a, torch, P, dist, world, rank, T, ix, q)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
+    batched = None if (a.no_batch or world > 1) else run_batched(a, torch, P, lib, ctypes)
     pk, pk_kind = peaks()
     bytes_steps = [step_bytes(ix, o, s_w) for o in outs]
     mean_bytes = float(np.mean(bytes_steps))
@@ -365,6 +469,10 @@ def run_ours(a):
         "gpu_launches": int(sum(1 + w for w in waves)),
         "clocks": clk.summary(),
     }
+    if batched is not None:
+        line["batched_c3"] = batched
+    if sharded is not None:
+        line["sharded"] = sharded
     if not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(T, ix, q[W:], cfg, a.cpu_seconds)
     print(json.dumps(line), flush=True)

@@ -98,6 +98,9 @@ struct csvd_ctx {
     long long *ids_pin_b = nullptr;
     double *logits_pin_b = nullptr;
     cudaEvent_t fork = nullptr;
+    double **d_Uraw_l = nullptr, **d_dots_l = nullptr;  // [lanes] per-lane bound outputs
+    void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *) = nullptr;
+    size_t kbb_smem = 0;
     cudaGraphExec_t g_batch = nullptr;
     int g_batch_B = 0, g_batch_host = 0;
 };
@@ -398,6 +401,29 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
     }
     if (!ctx->fork) CK(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    // shared batched bounds: regular bound plans (d = 2^m leaves of L % 8 == 0)
+    ctx->kbb = nullptr;
+    if (D0.bplan.regular && D0.bplan.cpl == 8 && D0.mode != CSVD_MODE_BIAS_AUGMENTED) {
+        switch (D0.bplan.q) {
+            case 1: ctx->kbb = k_bounds_batch<1>; break;
+            case 2: ctx->kbb = k_bounds_batch<2>; break;
+            case 4: ctx->kbb = k_bounds_batch<4>; break;
+        }
+    }
+    if (ctx->kbb) {
+        std::vector<double *> ur(B), dt(B);
+        for (int b = 0; b < B; ++b) {
+            ur[b] = ctx->lanes[b].D.Uraw;
+            dt[b] = ctx->lanes[b].D.dots;
+            ctx->lanes[b].D.pre_bounds = 1;
+        }
+        if ((rc = lalloc(ctx, &ctx->d_Uraw_l, B)) || (rc = lalloc(ctx, &ctx->d_dots_l, B))) return rc;
+        CK(cudaMemcpy(ctx->d_Uraw_l, ur.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_dots_l, dt.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
+        ctx->kbb_smem = sizeof(double) * BQN * (size_t)((pw_hs_size(D0.bplan) + 1) & ~1);
+        CK(cudaFuncSetAttribute((const void *)ctx->kbb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ctx->kbb_smem));
+    }
     ctx->lane_grid = G;
     ctx->lane_K = K;
     return 0;
@@ -414,6 +440,11 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     if (host_io)
         CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
+        ctx->kbb<<<ctx->grid, THREADS, ctx->kbb_smem, s>>>(D0, ctx->d_H, B, ctx->d_Uraw_l, ctx->d_dots_l,
+                                                           ctx->d_res_all);
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(ctx->fork, s));
     for (int b = 0; b < B; ++b) {
         Lane &l = ctx->lanes[b];
@@ -723,6 +754,7 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     CK(cudaMemset(D.st, 0, sizeof(ScanState)));
     CK(cudaMemset(D.res, 0, sizeof(csvd_result)));
     D.dbg = nullptr;
+    D.pre_bounds = 0;
     if (getenv("CSVD_DEBUG_TS") && atoi(getenv("CSVD_DEBUG_TS")) > 0) {
         if ((rc = dalloc(ctx, &D.dbg, 128))) return rc;
         CK(cudaMemset(D.dbg, 0, 128 * 8));

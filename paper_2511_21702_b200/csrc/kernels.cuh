@@ -78,6 +78,7 @@ struct Dev {
     unsigned *bar;           // grid barrier: [0] arrivals, [1] generation
     int nblocks;
     int launch_mode;
+    int pre_bounds;          // 1: Uraw / dots / query_norm come from k_bounds_batch
     int hs_off_b;            // offset (doubles) of the bounds h layout, 0 = shared with W
     int scratch_off;         // generic-path per-warp leaf scratch
     int ord_off;             // ordering arrays (rank staging, then order/cum/Uo/lrh)
@@ -1222,12 +1223,12 @@ static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, Sc
 }
 
 // fast path eligibility: the head is the first wave of an incremental step
-// with a top-k target under the default wave policy
+// under the default wave policy.  The head is an exact prefix of the order
+// whatever the targets; for softmax / top-p targets it is just a good guess
+// of where certification happens (if not, the full order is built and the
+// scan continues past it).
 __device__ __forceinline__ bool head_eligible(const csvd_config &cfg) {
-    if (cfg.variant != CSVD_VARIANT_INCREMENTAL || cfg.first_wave_tokens > 0) return false;
-    for (int t = 0; t < cfg.n_targets; ++t)
-        if (cfg.targets[t] == CSVD_TARGET_TOPK) return true;
-    return false;
+    return cfg.variant == CSVD_VARIANT_INCREMENTAL && cfg.first_wave_tokens <= 0;
 }
 
 // after a wave's scan: done / dense / next wave (thread 0): done / dense / next wave (thread 0)
@@ -1381,8 +1382,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
     if (lead) DBG_TS(D, 0);
     if (D.launch_mode != LAUNCH_BOUNDS) pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
-    if (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b) pw_stage<BCPL>(D.bplan, D.h, D.d, hs_b, D.bsrc);
-    if (D.launch_mode != LAUNCH_DENSE && lane == 0) {
+    if (!D.pre_bounds && (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b))
+        pw_stage<BCPL>(D.bplan, D.h, D.d, hs_b, D.bsrc);
+    if (D.launch_mode != LAUNCH_DENSE && !D.pre_bounds && lane == 0) {
         // start the HBM reads of this warp's centroid rows (and, in CTA 0, the
         // per-cluster arrays every CTA reads later) while h is staged
         const int c = warp * gridDim.x + blockIdx.x;
@@ -1414,9 +1416,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             D.res->slack = 0.0;
         }
     } else {
-        bounds_phase<BCPL, BQ>(D, hs_b, scratch);
-        if (lead) DBG_TS(D, 2);
-        grid_sync(D);
+        if (!D.pre_bounds) {
+            bounds_phase<BCPL, BQ>(D, hs_b, scratch);
+            if (lead) DBG_TS(D, 2);
+            grid_sync(D);
+        }
         if (lead) DBG_TS(D, 3);
         const bool ok = stage_bounds(D, o);
         if (!ok || D.launch_mode == LAUNCH_BOUNDS) {
@@ -1511,5 +1515,57 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             }
             break;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// batched bounds (decode over a batch): U for B queries with every centroid
+// row read once per group of BQN queries (warp per cluster, the same pairwise
+// tree per query as bounds_phase); lanes then start from these bounds.
+// Regular plans only (the bound dimension is d: euclidean / spherical).
+// ---------------------------------------------------------------------------
+#define BQN 4
+template <int BQ>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_bounds_batch(Dev D, const double *__restrict__ H, int B, double *const *Uraw_l, double *const *dots_l,
+                   csvd_result *res_all) {
+    extern __shared__ __align__(16) double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hs_stride = (pw_hs_size(D.bplan) + 1) & ~1;
+    __shared__ double s_qn[BQN];
+    const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
+    for (int qb = 0; qb < B; qb += BQN) {
+        const int nq = min(BQN, B - qb);
+        for (int j = 0; j < nq; ++j) pw_stage<8>(D.bplan, H + (size_t)(qb + j) * D.d, D.d, smem + j * hs_stride, nullptr);
+        __syncthreads();
+        if (warp < nq) {  // ||h|| (_linalg.py:40-43)
+            const double *hs = smem + warp * hs_stride;
+            const double ss = warp_dot_t<double, 8, BQ>(H + (size_t)(qb + warp) * D.d, hs, D.bplan, nullptr, lane);
+            const double qn = __dsqrt_rn(ss);
+            if (lane == 0) {
+                s_qn[warp] = qn;
+                if (blockIdx.x == 0) res_all[qb + warp].query_norm = qn;
+            }
+        }
+        __syncthreads();
+        for (int c = gwarp; c < D.C; c += nwarps) {
+            double dots[BQN];
+            warp_dot_regular_multi<BQ, BQN>(D.cent + (size_t)c * D.bd, smem, hs_stride, nq, D.bplan.leaf_len, lane,
+                                            dots);
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < BQN; ++j) {
+                    if (j < nq) {
+                        const double dot = dots[j], qn = s_qn[j];
+                        const double u = (D.mode == CSVD_MODE_SPHERICAL)
+                                             ? cone_bound(D, c, dot, qn)
+                                             : __dadd_rn(__dadd_rn(dot, __dmul_rn(D.radii[c], qn)), D.maxb[c]);
+                        Uraw_l[qb + j][c] = u;
+                        dots_l[qb + j][c] = dot;
+                    }
+                }
+            }
+        }
+        __syncthreads();
     }
 }
