@@ -174,6 +174,34 @@ static __device__ __noinline__ void lse_combine(double &m, double &s, double m2,
     }
 }
 
+// exp(x) for x <= 0, inline and short (for log-sum-exp accumulations, where
+// the reference's own numpy SIMD exp is only ulp-accurate too): x = k ln2 + r,
+// |r| <= ln2/2, degree-13 Taylor polynomial in Horner form with explicit
+// FMAs (relative error ~2 ulp), 2^k by exponent arithmetic.  Returns 0 below
+// -708 (a term 1e-308 times the largest one of its sum).
+__device__ __forceinline__ double exp_nonpos(double x) {
+    if (!(x >= -708.0)) return 0.0;  // also -inf / NaN-free inputs -> 0
+    const double k = rint(__dmul_rn(x, 1.4426950408889634));
+    double r = __fma_rn(k, -6.93147180369123816490e-01, x);
+    r = __fma_rn(k, -1.90821492927058770002e-10, r);
+    double p = 1.0 / 6227020800.0;  // 1/13!
+    p = __fma_rn(p, r, 1.0 / 479001600.0);
+    p = __fma_rn(p, r, 1.0 / 39916800.0);
+    p = __fma_rn(p, r, 1.0 / 3628800.0);
+    p = __fma_rn(p, r, 1.0 / 362880.0);
+    p = __fma_rn(p, r, 1.0 / 40320.0);
+    p = __fma_rn(p, r, 1.0 / 5040.0);
+    p = __fma_rn(p, r, 1.0 / 720.0);
+    p = __fma_rn(p, r, 1.0 / 120.0);
+    p = __fma_rn(p, r, 1.0 / 24.0);
+    p = __fma_rn(p, r, 1.0 / 6.0);
+    p = __fma_rn(p, r, 0.5);
+    p = __fma_rn(p, r, 1.0);
+    p = __fma_rn(p, r, 1.0);
+    const long long ki = (long long)k;  // in [-1022, 0]
+    return __longlong_as_double(__double_as_longlong(p) + (ki << 52));
+}
+
 // strict total order of the opening sequence: U descending, id ascending
 // (np.lexsort((arange(C), -U)), decode.py:166)
 __device__ __forceinline__ bool key_before(double ua, int ia, double ub, int ib) {
@@ -332,10 +360,25 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) 
     const csvd_config &cfg = *D.cfg;
     __shared__ double s_red[WARPS];
     double *__restrict__ Us = o.Us;
+    // by cluster id, for the head path: x = log|c| (+ U below) in the keys
+    // region, the best-logit estimate in Uo, |c| in cum (all loads in flight
+    // together; order_full rebuilds these regions from global memory)
+    double *__restrict__ xs = reinterpret_cast<double *>(o.keys);
+    double *__restrict__ es = o.Uo;
+    int *__restrict__ zs = o.cum;
+    const bool aug = D.mode == CSVD_MODE_BIAS_AUGMENTED;
     double amax = 1.0;
+#pragma unroll 4
     for (int c = tid; c < C; c += THREADS) {
         const double u = __ldcg(D.Uraw + c);
+        const double dt = __ldcg(D.dots + c);
+        const double mb = __ldg(D.meanb + c);
+        const double lz = __ldg(D.logsz + c);
+        const int sz = __ldg(D.sizes + c);
         Us[c] = u;
+        es[c] = aug ? dt : __dadd_rn(dt, mb);  // init_state's estimate of the best logit
+        xs[c] = lz;
+        zs[c] = sz;
         amax = fmax(amax, fabs(u));
     }
     double eta = 0.0;
@@ -348,6 +391,7 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) 
         const double u = __dadd_rn(Us[c], eta);
         bad |= !isfinite(u);  // BoundVector.__post_init__ (bounds.py:53-55)
         Us[c] = u;
+        xs[c] = __dadd_rn(xs[c], u);  // certify.py:119 np.log(sizes) + U
         if (blockIdx.x == 0) D.U[c] = u;
     }
     bad = __syncthreads_or(bad);
@@ -417,8 +461,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
                 bi = s_i[w];
             }
         s_i[0] = bi;
-        const double dt = __ldcg(D.dots + bi);  // init_state's estimate of the best logit
-        s_est = (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? dt : __dadd_rn(dt, __ldg(D.meanb + bi));
+        s_est = o.Uo[bi];  // estimate by id (stage_bounds)
     }
     __syncthreads();
     const int c0 = s_i[0];
@@ -429,9 +472,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
     bi = 0x7fffffff;
     for (int c = tid; c < C; c += THREADS) {
         const double u = Us[c];
-        const double x = __dadd_rn(__ldg(D.logsz + c), u);
-        xs[c] = x;
-        xm = fmax(xm, x);
+        xm = fmax(xm, xs[c]);
         if (u >= est || c == c0) {
             const int slot = atomicAdd(&s_n, 1);
             if (slot < 64) s_head[slot] = c;
@@ -467,7 +508,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
     // --- residual mass of everything outside the head
     double rest = 0.0;
     for (int c = tid; c < C; c += THREADS)
-        if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, csvd_exp(__dsub_rn(xs[c], xmax)));
+        if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, exp_nonpos(__dsub_rn(xs[c], xmax)));
     rest = warp_sum(rest);
     __syncthreads();  // s_x reuse
     if (lane == 0) s_x[warp] = rest;
@@ -518,9 +559,10 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
             }
         }
         // positions lane (a) and lane + 32 (b): order, Uo, cum, lrh
-        const int sa = lane < n ? __ldg(D.sizes + ia) : 0, sb = lane + 32 < n ? __ldg(D.sizes + ib) : 0;
-        const double ea = lane < n ? csvd_exp(__dsub_rn(xs[ia], xmax)) : 0.0;
-        const double eb = lane + 32 < n ? csvd_exp(__dsub_rn(xs[ib], xmax)) : 0.0;
+        const int sa = lane < n ? o.cum[ia] : 0, sb = lane + 32 < n ? o.cum[ib] : 0;  // |c| by id
+        __syncwarp();  // cum is rewritten by position below
+        const double ea = lane < n ? exp_nonpos(__dsub_rn(xs[ia], xmax)) : 0.0;
+        const double eb = lane + 32 < n ? exp_nonpos(__dsub_rn(xs[ib], xmax)) : 0.0;
         int ca = sa, cb = sb;  // inclusive prefix sums
         double ra = ea, rb = eb;  // inclusive suffix sums
 #pragma unroll
@@ -650,7 +692,7 @@ static __device__ __forceinline__ void order_full(const Dev &D, const Ord &o) {
     for (int p = b0; p < b1; ++p) {
         o.cum[p] = run;
         run += __ldg(D.sizes + o.order[p]);
-        const double e = csvd_exp(__dsub_rn(x[p], xmax));
+        const double e = exp_nonpos(__dsub_rn(x[p], xmax));
         o.Us[p] = e;  // Us by id is dead: reuse as e by position
     }
     for (int p = b1 - 1; p >= b0; --p) tail = __dadd_rn(tail, o.Us[p]);
@@ -927,13 +969,13 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
         if (M == -INFINITY) {
             lz = -INFINITY;
         } else {
-            double t = (act && lse_q != -INFINITY) ? csvd_exp(__dsub_rn(lse_q, M)) : 0.0;
+            double t = (act && lse_q != -INFINITY) ? exp_nonpos(__dsub_rn(lse_q, M)) : 0.0;
 #pragma unroll
             for (int s = 1; s < 32; s <<= 1) {
                 const double u = __shfl_up_sync(CSVD_FULL, t, s);
                 if (lane >= s) t = __dadd_rn(t, u);
             }
-            if (st0.log_z != -INFINITY) t = __dadd_rn(t, csvd_exp(__dsub_rn(st0.log_z, M)));
+            if (st0.log_z != -INFINITY) t = __dadd_rn(t, exp_nonpos(__dsub_rn(st0.log_z, M)));
             lz = t > 0.0 ? __dadd_rn(M, csvd_log(t)) : -INFINITY;
         }
     }
