@@ -1156,8 +1156,19 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
     double lv = -INFINITY;  // small k: lane l holds the l-th largest so far
     int cnt = 0;
     double kmin = -INFINITY;
+    // rows stream through L2: lane 0 keeps the warp's next PD rows in flight
+    // with bulk prefetches, so HBM sees ~PD x 1184 rows of requests at all times
+    constexpr int PD = 2;
+    const size_t rb = (size_t)D.d * sizeof(ET);
+    if (lane == 0)
+        for (int j = 0; j < PD; ++j) {
+            const int r = gwarp + j * nwarps;
+            if (r < D.Vl) bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)r * rb, rb);
+        }
     for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
         const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
+        if (lane == 0 && lr + PD * nwarps < D.Vl)
+            bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(lr + PD * nwarps) * rb, rb);
         const double logit = row_logit<ET, CPL, Q>(D, lr, pos, hs, scratch, lane);
         if (lane == 0) {
             const int tok = __ldg(D.perm + pos);
