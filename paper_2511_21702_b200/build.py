@@ -24,7 +24,7 @@ NVCC_FLAGS = [
     "-fmad=false",            # belt and braces: the kernels use __dmul_rn/__dadd_rn anyway
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
-    "-diag-suppress", "20279",  # extern __global__ templates (kinst.cu instantiates them)
+    "-diag-suppress", "20279,20281",  # extern __global__ templates (kinst.cu instantiates them)
 ]
 
 # step-kernel instantiations: (weight element type, chains per lane, slices);

@@ -127,6 +127,48 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *p, size_t bytes) {
     }
 }
 
+// ---- TMA bulk copies (global -> shared, completion on an mbarrier) ----------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// Stage nq query vectors (leaf layout of a CPL = 8 plan: leaf_len doubles per
+// leaf, 2-double pad) with one bulk copy per leaf, issued by warp 0; every
+// thread returns once the bytes have landed.  `phase` = completions so far.
+__device__ __forceinline__ void tma_stage_leaves(const PwPlan &pl, const double *H, int d, int nq, double *hs,
+                                                 int hs_stride, unsigned long long *bar, unsigned phase) {
+    const int L = pl.leaf_len, nl = pl.nleaf;
+    if (threadIdx.x < 32) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of hs
+        if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(nq * nl * L * 8));
+        __syncwarp();
+        for (int t = threadIdx.x; t < nq * nl; t += 32) {
+            const int j = t / nl, leaf = t - j * nl;
+            bulk_g2s(hs + (size_t)j * hs_stride + (size_t)leaf * (L + 2), H + (size_t)j * d + (size_t)leaf * L,
+                     (unsigned)(L * 8), bar);
+        }
+    }
+    mbar_wait(bar, phase & 1u);
+}
+
 __device__ __forceinline__ unsigned long long dkey(double v) {
     unsigned long long u = (unsigned long long)__double_as_longlong(v);
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
@@ -266,6 +308,12 @@ __device__ __forceinline__ double cone_bound(const Dev &D, int c, double dot, do
     return __dadd_rn(geom, D.maxb[c]);
 }
 
+// U from a centroid dot (batch lanes; off the single-query path, so out of line)
+static __device__ __noinline__ double bound_from_dot(const Dev &D, int c, double dot, double qn) {
+    if (D.mode == CSVD_MODE_SPHERICAL) return cone_bound(D, c, dot, qn);
+    return __dadd_rn(__dadd_rn(dot, __dmul_rn(D.radii[c], qn)), D.maxb[c]);
+}
+
 template <int BCPL, int BQ>
 __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -354,7 +402,7 @@ __device__ __forceinline__ double block_max(double v, double *red) {
 // Stage U + slack (bounds.py:58-64, which needs max |U| first) by cluster id
 // in shared memory; CTA 0 publishes it for cluster_bounds (bounds.py:178-184).
 // Returns false (in every CTA) if a bound is non-finite.
-static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) {
+static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, double qn_given) {
     const int tid = threadIdx.x;
     const int C = D.C;
     const csvd_config &cfg = *D.cfg;
@@ -368,10 +416,7 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) 
     int *__restrict__ zs = o.cum;
     const bool aug = D.mode == CSVD_MODE_BIAS_AUGMENTED;
     double amax = 1.0;
-#pragma unroll 4
-    for (int c = tid; c < C; c += THREADS) {
-        const double u = __ldcg(D.Uraw + c);
-        const double dt = __ldcg(D.dots + c);
+    auto put = [&](int c, double u, double dt) {
         const double mb = __ldg(D.meanb + c);
         const double lz = __ldg(D.logsz + c);
         const int sz = __ldg(D.sizes + c);
@@ -380,6 +425,16 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o) 
         xs[c] = lz;
         zs[c] = sz;
         amax = fmax(amax, fabs(u));
+    };
+    if (!D.pre_bounds) {
+#pragma unroll 4
+        for (int c = tid; c < C; c += THREADS) put(c, __ldcg(D.Uraw + c), __ldcg(D.dots + c));
+    } else {  // batched bounds: U from the given dots (bounds.py:79-83 / 95-118) and this lane's ||h||
+#pragma unroll 1
+        for (int c = tid; c < C; c += THREADS) {
+            const double dt = __ldcg(D.dots + c);
+            put(c, bound_from_dot(D, c, dt, qn_given), dt);
+        }
     }
     double eta = 0.0;
     if (cfg.slack_f32) {
@@ -1419,6 +1474,20 @@ static __device__ void shard_dense_list(const Dev &D, double kth, int k) {
     }
 }
 
+// batch lanes: ||h|| from the staged copy (out of line: off the single-query path)
+template <int BQ>
+static __device__ __noinline__ void lane_query_norm(const Dev &D, const double *hs, double &out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        const double qn = __dsqrt_rn(warp_selfdot_smem<BQ>(hs, D.bplan.leaf_len, lane));
+        if (lane == 0) {
+            out = qn;
+            if (blockIdx.x == 0) D.res->query_norm = qn;
+        }
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // the step kernel
 // ---------------------------------------------------------------------------
@@ -1473,9 +1542,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             bounds_phase<BCPL, BQ>(D, hs_b, scratch);
             if (lead) DBG_TS(D, 2);
             grid_sync(D);
+        } else if constexpr (BCPL == 8) {  // batched bounds: dots are given; ||h|| here
+            lane_query_norm<BQ>(D, hs_b, ss.st.est);  // carried to stage_bounds (ss is rebuilt later)
         }
         if (lead) DBG_TS(D, 3);
-        const bool ok = stage_bounds(D, o);
+        const bool ok = stage_bounds(D, o, ss.st.est);
         if (!ok || D.launch_mode == LAUNCH_BOUNDS) {
             if (lead) D.res->error = ok ? 0 : CSVD_EVALUE;
             return;
@@ -1585,38 +1656,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hs_stride = (pw_hs_size(D.bplan) + 1) & ~1;
-    __shared__ double s_qn[BQN];
+    __shared__ unsigned long long s_bar;
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
     const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
+    if (lane == 0)  // this warp's centroid rows start streaming into L2 (later passes hit there)
+        for (int c = gwarp; c < D.C; c += nwarps) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
     for (int qb = 0; qb < B; qb += BQN) {
         const int nq = min(BQN, B - qb);
-        for (int j = 0; j < nq; ++j) pw_stage<8>(D.bplan, H + (size_t)(qb + j) * D.d, D.d, smem + j * hs_stride, nullptr);
-        __syncthreads();
-        if (warp < nq) {  // ||h|| (_linalg.py:40-43)
-            const double *hs = smem + warp * hs_stride;
-            const double ss = warp_dot_t<double, 8, BQ>(H + (size_t)(qb + warp) * D.d, hs, D.bplan, nullptr, lane);
-            const double qn = __dsqrt_rn(ss);
-            if (lane == 0) {
-                s_qn[warp] = qn;
-                if (blockIdx.x == 0) res_all[qb + warp].query_norm = qn;
-            }
-        }
-        __syncthreads();
+        tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / BQN));
         for (int c = gwarp; c < D.C; c += nwarps) {
             double dots[BQN];
             warp_dot_regular_multi<BQ, BQN>(D.cent + (size_t)c * D.bd, smem, hs_stride, nq, D.bplan.leaf_len, lane,
                                             dots);
-            if (lane == 0) {
+            if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
 #pragma unroll
-                for (int j = 0; j < BQN; ++j) {
-                    if (j < nq) {
-                        const double dot = dots[j], qn = s_qn[j];
-                        const double u = (D.mode == CSVD_MODE_SPHERICAL)
-                                             ? cone_bound(D, c, dot, qn)
-                                             : __dadd_rn(__dadd_rn(dot, __dmul_rn(D.radii[c], qn)), D.maxb[c]);
-                        Uraw_l[qb + j][c] = u;
-                        dots_l[qb + j][c] = dot;
-                    }
-                }
+                for (int j = 0; j < BQN; ++j)
+                    if (j < nq) dots_l[qb + j][c] = dots[j];
             }
         }
         __syncthreads();

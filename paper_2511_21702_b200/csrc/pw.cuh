@@ -245,7 +245,7 @@ template <int Q, int NQ>
 __device__ __forceinline__ void warp_dot_regular_multi(const double *__restrict__ row,
                                                        const double *__restrict__ hs0, int hs_stride, int nq,
                                                        int leaf_len, int lane, double (&out)[NQ]) {
-    constexpr int NB = 2;
+    constexpr int NB = 4;
     const int S = leaf_len >> 3;
     double slice[NQ][Q];
 #pragma unroll
@@ -307,6 +307,41 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *__restrict_
             tot = d_add(d_add(slice[j][0], slice[j][1]), d_add(slice[j][2], slice[j][3]));
         out[j] = d_add(0.0, tot);
     }
+}
+
+// ||h||^2 in the CPL = 8 pairwise order with both operands from the staged
+// shared-memory copy (same tree as warp_dot_regular<double, 8, Q>(h, hs)).
+template <int Q>
+__device__ __forceinline__ double warp_selfdot_smem(const double *__restrict__ hs, int leaf_len, int lane) {
+    const int S = leaf_len >> 3;
+    double slice[Q];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+        const double *hp = hs + (size_t)(u * 32 + lane) * (leaf_len + 2);
+        double r[8];
+        for (int i = 0; i < S; ++i) {
+            const double2 *h2 = reinterpret_cast<const double2 *>(hp + 8 * i);
+#pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) {
+                const double2 t = h2[c2];
+                const double p0 = d_mul(t.x, t.x), p1 = d_mul(t.y, t.y);
+                r[2 * c2] = (i == 0) ? p0 : d_add(r[2 * c2], p0);
+                r[2 * c2 + 1] = (i == 0) ? p1 : d_add(r[2 * c2 + 1], p1);
+            }
+        }
+        double v = d_add(d_add(d_add(r[0], r[1]), d_add(r[2], r[3])), d_add(d_add(r[4], r[5]), d_add(r[6], r[7])));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
+        slice[u] = v;
+    }
+    double tot;
+    if constexpr (Q == 1)
+        tot = slice[0];
+    else if constexpr (Q == 2)
+        tot = d_add(slice[0], slice[1]);
+    else
+        tot = d_add(d_add(slice[0], slice[1]), d_add(slice[2], slice[3]));
+    return d_add(0.0, tot);
 }
 
 // host: source element of interleaved index idx (CPL < 8 plans)
