@@ -37,6 +37,8 @@ from .engine import (
     prepare,
 )
 from .shard import CommLedger, LatencyModel, ShardPlan, make_plan, sharded_decode_step
+from .budget import (AdaptiveBudget, BudgetedDecoder, FlopReport, adapt_budget, flop_accounting, flop_report,
+                     warmup_k_max)
 
 __version__ = "0.1.0"
 
@@ -45,5 +47,6 @@ __all__ = [
     "DecodeOutcome", "DenseResult", "EmbeddingTable", "FingerprintMismatchError", "FullVocab",
     "PartialExpand", "RelaxEps", "StepMetrics", "DeviceIndex", "clear_cache", "cluster_bounds",
     "decode_step", "decode_step_batch", "decode_step_batchselect", "dense_logits", "prepare", "CommLedger",
-    "LatencyModel", "ShardPlan", "make_plan", "sharded_decode_step",
+    "LatencyModel", "ShardPlan", "make_plan", "sharded_decode_step", "AdaptiveBudget", "BudgetedDecoder",
+    "FlopReport", "adapt_budget", "flop_accounting", "flop_report", "warmup_k_max",
 ]

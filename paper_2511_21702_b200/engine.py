@@ -142,6 +142,7 @@ class DeviceIndex:
             self._ctx = None
             _raise(rc, msg)
         self._lib = lib
+        self._cfg_cache = {}
         self._lock = threading.Lock()
         self._res = _lib.Result()
         self._ids = np.empty(self.V, dtype=np.int64)
@@ -172,7 +173,19 @@ class DeviceIndex:
     # --- config -----------------------------------------------------------
     def make_config(self, cfg, k_max=None, variant=_lib.VARIANT_INCREMENTAL,
                     first_wave_tokens: int = 0) -> _lib.Config:
-        return config_struct(cfg, self.V, k_max, variant, first_wave_tokens)
+        """csvd_config for `cfg`; memoized per (frozen, hashable) config since
+        validating and flattening it costs more host time than the launch."""
+        try:
+            key = (cfg, k_max, variant, first_wave_tokens)
+            hit = self._cfg_cache.get(key)
+        except TypeError:  # unhashable config object
+            return config_struct(cfg, self.V, k_max, variant, first_wave_tokens)
+        if hit is None:
+            hit = config_struct(cfg, self.V, k_max, variant, first_wave_tokens)
+            if len(self._cfg_cache) > 256:
+                self._cfg_cache.clear()
+            self._cfg_cache[key] = hit
+        return hit
 
     # --- step -------------------------------------------------------------
     def step(self, h, cfg, k_max=None, variant=_lib.VARIANT_INCREMENTAL) -> DecodeOutcome:

@@ -140,3 +140,23 @@ def test_head_fast_path_and_general_path_agree():
                 assert c.variant == _lib.VARIANT_INCREMENTAL
                 got = ctx.step(h, c)
                 assert_outcome(got, e, rtol=TRANS_RTOL, where=f"head[{ci},{i},fwt={fwt}]")
+
+
+def test_budgeted_decoder_sequence_matches_oracle():
+    """The adaptive budget in front of the step (decode.py:404-431): the same
+    controller trajectory and outcomes as the oracle run with the controller's
+    k_max, over a query stream that mixes certified steps and fallbacks."""
+    T, ix = _c1_like(V=32000, d=4096, n_modes=64, g=4)
+    q = np.vstack([wl.generate_queries(10, 4096, "contextual", 7, centroids=ix.centroids),
+                   wl.generate_queries(3, 4096, "random", 8)])
+    cfg = P.DecodeConfig(k=10, adaptive_enabled=True, alpha=0.5, rho_target=0.05, ema_half_life=3.0,
+                         warmup_steps=2)
+    dec = P.BudgetedDecoder(T, ix, cfg, initial_k_max=700)
+    ctl = P.AdaptiveBudget(cfg, ix.vocab_size, 700)
+    for t, h in enumerate(q):
+        km = ctl.effective_k_max(t)
+        exp = O.decode_step(T, ix, h, cfg, k_max=km)
+        got = dec.step(h)
+        assert_outcome(got, _fields(exp), rtol=TRANS_RTOL, where=f"budget[{t}] k_max={km}")
+        ctl.observe(exp.fallback_used is not None)
+        assert dec.ctl.k_max == ctl.k_max
