@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -75,6 +76,13 @@ struct csvd_ctx {
     long long *ids_pin = nullptr;
     double *logits_pin = nullptr;
     cudaGraphExec_t g_step = nullptr, g_host = nullptr, g_bounds = nullptr, g_dense = nullptr;
+    // zero-copy host results (csvd_step_host): mapped pinned buffers + flag
+    csvd_result *res_map = nullptr;
+    long long *ids_map = nullptr;
+    double *logits_map = nullptr;
+    unsigned long long *flag_map = nullptr;
+    unsigned long long seq_host = 0;
+    Dev Dhost{};
     int direct = 0;
     void *flush_buf = nullptr;
     int64_t first_chunk = 0;
@@ -278,8 +286,8 @@ static int configure(csvd_ctx *ctx) {
     return 0;
 }
 
-static int launch(csvd_ctx *ctx, int mode, cudaStream_t s) {
-    Dev D = ctx->D;
+static int launch(csvd_ctx *ctx, int mode, cudaStream_t s, bool host_map = false) {
+    Dev D = host_map ? ctx->Dhost : ctx->D;
     D.launch_mode = mode;
     void *args[] = {&D};
     CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->grid), dim3(THREADS), args, ctx->smem, s));
@@ -292,16 +300,11 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
-    int rc = launch(ctx, mode, s);
+    // host I/O: the kernel itself writes the result into mapped host memory
+    int rc = launch(ctx, mode, s, host_io);
     if (rc) {
         cudaStreamEndCapture(s, &g);
         return rc;
-    }
-    if (host_io) {
-        const int64_t first = ctx->first_chunk;
-        CK(cudaMemcpyAsync(ctx->res_pin, ctx->D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(ctx->ids_pin, ctx->D.S_ids, sizeof(long long) * first, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(ctx->logits_pin, ctx->D.S_logits, sizeof(double) * first, cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamEndCapture(s, &g));
     CK(cudaGraphInstantiate(out, g, 0));
@@ -310,6 +313,19 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
 }
 
 static int build_graphs(csvd_ctx *ctx) {
+    {  // the host-API variant of the per-step Dev: mapped result buffers
+        Dev &H = ctx->Dhost;
+        H = ctx->D;
+        void *p = nullptr;
+        CK(cudaHostGetDevicePointer(&p, ctx->res_map, 0));
+        H.res_host = (csvd_result *)p;
+        CK(cudaHostGetDevicePointer(&p, ctx->ids_map, 0));
+        H.ids_host = (long long *)p;
+        CK(cudaHostGetDevicePointer(&p, ctx->logits_map, 0));
+        H.logits_host = (double *)p;
+        CK(cudaHostGetDevicePointer(&p, ctx->flag_map, 0));
+        H.host_flag = (volatile unsigned long long *)p;
+    }
     for (cudaGraphExec_t *g : {&ctx->g_step, &ctx->g_host, &ctx->g_bounds, &ctx->g_dense}) {
         if (*g) cudaGraphExecDestroy(*g);
         *g = nullptr;
@@ -768,6 +784,19 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     CK(cudaHostAlloc(&ctx->ids_pin, sizeof(long long) * V, cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->logits_pin, sizeof(double) * V, cudaHostAllocDefault));
     memset(ctx->cfg_pin, 0, sizeof(csvd_config));
+    CK(cudaHostAlloc(&ctx->res_map, sizeof(csvd_result), cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->ids_map, sizeof(long long) * V, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->logits_map, sizeof(double) * V, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->flag_map, sizeof(unsigned long long), cudaHostAllocMapped));
+    *ctx->flag_map = 0;
+    D.res_host = nullptr;
+    D.ids_host = nullptr;
+    D.logits_host = nullptr;
+    D.host_flag = nullptr;
+    if ((rc = dalloc(ctx, &D.done_ctas, 1))) return rc;
+    if ((rc = dalloc(ctx, &D.seq, 1))) return rc;
+    CK(cudaMemset(D.done_ctas, 0, sizeof(unsigned)));
+    CK(cudaMemset(D.seq, 0, sizeof(unsigned long long)));
     D.K = 32;
     if ((rc = configure(ctx))) return rc;
     if ((rc = alloc_k(ctx, 32))) return rc;
@@ -802,6 +831,8 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     if (ctx->res_pin) cudaFreeHost(ctx->res_pin);
     if (ctx->ids_pin) cudaFreeHost(ctx->ids_pin);
     if (ctx->logits_pin) cudaFreeHost(ctx->logits_pin);
+    for (void *p : {(void *)ctx->res_map, (void *)ctx->ids_map, (void *)ctx->logits_map, (void *)ctx->flag_map})
+        if (p) cudaFreeHost(p);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return 0;
@@ -876,7 +907,39 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         CK(cudaMemcpyAsync(ctx->ids_pin, ctx->D.S_ids, sizeof(long long) * first, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->logits_pin, ctx->D.S_logits, sizeof(double) * first, cudaMemcpyDeviceToHost, s));
     } else {
+        // zero-copy: the kernel writes ids / logits / result into mapped host
+        // memory and raises the flag; spin on it instead of a stream sync
+        const unsigned long long want = ++ctx->seq_host;
         CK(cudaGraphLaunch(ctx->g_host, s));
+        volatile unsigned long long *flag = ctx->flag_map;
+        bool got = false;
+        for (unsigned long long spins = 0;; ++spins) {
+            if (*flag == want) {
+                got = true;
+                break;
+            }
+            if ((spins & 255) == 255 && cudaStreamQuery(s) != cudaErrorNotReady) {
+                got = *flag == want;
+                break;
+            }
+        }
+        if (got) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            memcpy(res, (const void *)ctx->res_map, sizeof(csvd_result));
+            if ((rc = result_error(ctx, *res))) return rc;
+            const int64_t n = res->sub_size;
+            if (n > cap) return fail(ctx, CSVD_EDIM, "output capacity too small");
+            if (ids) memcpy(ids, ctx->ids_map, sizeof(int64_t) * n);
+            if (logits) memcpy(logits, ctx->logits_map, sizeof(double) * n);
+            return 0;
+        }
+        // the step ended without publishing (device error): read its state
+        --ctx->seq_host;
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(ctx->res_pin, ctx->D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost));
+        *res = *ctx->res_pin;
+        if ((rc = result_error(ctx, *res))) return rc;
+        return fail(ctx, CSVD_ESTATE, "step finished without publishing its result");
     }
     CK(cudaStreamSynchronize(s));
     *res = *ctx->res_pin;

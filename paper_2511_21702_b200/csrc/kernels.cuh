@@ -61,6 +61,14 @@ struct Dev {
     int Vl;
     int *order_g, *cum_g;    // shard opens: the opening order / prefix counts for the host
     double *shard_out;       // CSVD_SH_* aggregate (K + CSVD_SH_TOPK doubles)
+    // host-API steps: the result lands directly in mapped pinned host memory
+    // (no copy nodes); the last CTA to finish its slice raises `host_flag`
+    csvd_result *res_host;   // null: device-resident step
+    long long *ids_host;
+    double *logits_host;
+    volatile unsigned long long *host_flag;
+    unsigned *done_ctas;     // arrival counter for the copy-out
+    unsigned long long *seq; // step sequence number (device copy, bumped by the last CTA)
     PwPlan wplan, bplan;
     const int *wsrc, *bsrc;  // interleaved-layout source tables (CPL < 8 plans)
     // per step
@@ -1339,6 +1347,32 @@ __device__ __forceinline__ bool head_eligible(const csvd_config &cfg) {
     return cfg.variant == CSVD_VARIANT_INCREMENTAL && cfg.first_wave_tokens <= 0;
 }
 
+// host-API steps: every CTA copies its slice of the final outputs to the
+// mapped host buffers; the last to arrive publishes the result struct and the
+// sequence number the host is spinning on.
+static __device__ __noinline__ void publish_host(const Dev &D, long long n, const csvd_result *r_cta0) {
+    if (!D.res_host) return;
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long a = (long long)blockIdx.x * per, b = min(n, a + per);
+    for (long long i = a + threadIdx.x; i < b; i += THREADS) {
+        D.ids_host[i] = __ldcg(D.S_ids + i);
+        D.logits_host[i] = __ldcg(D.S_logits + i);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (r_cta0) *D.res_host = *r_cta0;
+        __threadfence_system();
+        const unsigned t = atomicAdd(D.done_ctas, 1u);
+        if (t == gridDim.x - 1) {
+            *D.done_ctas = 0;
+            const unsigned long long sq = *D.seq + 1;
+            *D.seq = sq;
+            __threadfence_system();
+            *D.host_flag = sq;
+        }
+    }
+}
+
 // after a wave's scan: done / dense / next wave (thread 0): done / dense / next wave (thread 0)
 static __device__ __forceinline__ void next_wave(const Dev &D, const Ord &o, ScanShared &ss) {
     ScanState s2 = ss.st;
@@ -1615,11 +1649,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             if (threadIdx.x == 0) next_wave(D, o, ss);
             if (lead) DBG_TS(D, 47);
             __syncthreads();
+            if (ss.st.mode == MODE_IDLE && D.res_host) {
+                csvd_result r = ss.res;
+                r.query_norm = D.res->query_norm;
+                r.slack = D.res->slack;
+                r.waves = ss.st.iter;
+                r.error = __ldcg(&D.res->error);
+                publish_host(D, r.sub_size, blockIdx.x == 0 ? &r : nullptr);
+            }
             if (lead) DBG_TS(D, 11 + 4 * (st.iter & 3));
         } else {  // MODE_DENSE
             dense_rows<ET, CPL, Q>(D, hs_w, scratch);
             grid_sync(D);
-            if (blockIdx.x != 0) break;
+            if (blockIdx.x != 0) {
+                publish_host(D, D.V, nullptr);
+                break;
+            }
             const double kth = block_kth_largest(D.cand, D.nblocks * WARPS * k, k, D.K, k);
             if (D.lpos) shard_dense_list(D, kth, k);
             if (threadIdx.x == 0) {
@@ -1636,7 +1681,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
                 *D.res = r;
                 s2.mode = MODE_IDLE;
                 *D.st = s2;
+                ss.res = r;
             }
+            __syncthreads();
+            publish_host(D, D.V, &ss.res);
             break;
         }
     }
