@@ -37,6 +37,7 @@ from .engine import (
     prepare,
 )
 from .shard import CommLedger, LatencyModel, ShardPlan, make_plan, sharded_decode_step
+from . import formats
 from .budget import (AdaptiveBudget, BudgetedDecoder, FlopReport, adapt_budget, flop_accounting, flop_report,
                      warmup_k_max)
 

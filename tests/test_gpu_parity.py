@@ -160,3 +160,17 @@ def test_budgeted_decoder_sequence_matches_oracle():
         assert_outcome(got, _fields(exp), rtol=TRANS_RTOL, where=f"budget[{t}] k_max={km}")
         ctl.observe(exp.fallback_used is not None)
         assert dec.ctl.k_max == ctl.k_max
+
+
+def test_files_to_device_step(tmp_path):
+    """CSVD + CSVI files -> mapped table + index -> resident context -> step."""
+    from paper_2511_21702_b200 import formats as F
+    T, ix = _c1_like(V=8000, d=512, n_modes=40, g=2)
+    F.save_table(T, tmp_path / "t.csvd")
+    F.save_index(ix, tmp_path / "i.csvi")
+    T2, ix2, ctx = F.prepare_files(tmp_path / "t.csvd", tmp_path / "i.csvi")
+    q = wl.generate_queries(3, 512, "contextual", 7, centroids=ix.centroids)
+    cfg = P.DecodeConfig(k=10)
+    for i, h in enumerate(q):
+        assert_outcome(P.decode_step(T2, ix2, h, cfg), _fields(O.decode_step(T, ix, h, cfg)), rtol=TRANS_RTOL,
+                       where=f"files[{i}]")
