@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -53,6 +54,7 @@ typedef void (*kern_t)(Dev);
 // through the shared L2) and own their per-step workspaces.
 struct Lane {
     Dev D{};
+    Dev Dh{};  // the same lane publishing into mapped host memory (host-API batches)
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
 };
@@ -111,6 +113,11 @@ struct csvd_ctx {
     size_t kbb_smem = 0;
     cudaGraphExec_t g_batch = nullptr;
     int g_batch_B = 0, g_batch_host = 0;
+    csvd_result *res_map_b = nullptr;  // [lanes] mapped
+    long long *ids_map_b = nullptr;    // [lanes, V] mapped
+    double *logits_map_b = nullptr;    // [lanes, V] mapped
+    unsigned long long *flags_b = nullptr;
+    unsigned long long batch_seq = 0;
 };
 
 static int fail(csvd_ctx *c, int code, const std::string &msg) {
@@ -357,6 +364,13 @@ static void free_lanes(csvd_ctx *ctx) {
     if (ctx->res_pin_b) cudaFreeHost(ctx->res_pin_b);
     if (ctx->ids_pin_b) cudaFreeHost(ctx->ids_pin_b);
     if (ctx->logits_pin_b) cudaFreeHost(ctx->logits_pin_b);
+    for (void *p : {(void *)ctx->res_map_b, (void *)ctx->ids_map_b, (void *)ctx->logits_map_b, (void *)ctx->flags_b})
+        if (p) cudaFreeHost(p);
+    ctx->res_map_b = nullptr;
+    ctx->ids_map_b = nullptr;
+    ctx->logits_map_b = nullptr;
+    ctx->flags_b = nullptr;
+    ctx->batch_seq = 0;
     ctx->H_pin = nullptr;
     ctx->res_pin_b = nullptr;
     ctx->ids_pin_b = nullptr;
@@ -392,6 +406,11 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     CK(cudaHostAlloc(&ctx->res_pin_b, sizeof(csvd_result) * B, cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->ids_pin_b, sizeof(long long) * B * first, cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->logits_pin_b, sizeof(double) * B * first, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->res_map_b, sizeof(csvd_result) * B, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->ids_map_b, sizeof(long long) * B * (size_t)V, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->logits_map_b, sizeof(double) * B * (size_t)V, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->flags_b, sizeof(unsigned long long) * B, cudaHostAllocMapped));
+    memset(ctx->flags_b, 0, sizeof(unsigned long long) * B);
     ctx->lanes.resize(B);
     for (int b = 0; b < B; ++b) {
         Lane &l = ctx->lanes[b];
@@ -412,7 +431,27 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemset(L.st, 0, sizeof(ScanState)));
         L.nblocks = G;
         L.dbg = nullptr;
+        L.res_host = nullptr;
+        L.ids_host = nullptr;
+        L.logits_host = nullptr;
+        L.host_flag = nullptr;
+        if ((rc = lalloc(ctx, &L.done_ctas, 1)) || (rc = lalloc(ctx, &L.seq, 1))) return rc;
+        CK(cudaMemset(L.done_ctas, 0, sizeof(unsigned)));
+        CK(cudaMemset(L.seq, 0, sizeof(unsigned long long)));
         l.D = L;
+        {
+            Dev Hl = L;
+            void *p = nullptr;
+            CK(cudaHostGetDevicePointer(&p, ctx->res_map_b + b, 0));
+            Hl.res_host = (csvd_result *)p;
+            CK(cudaHostGetDevicePointer(&p, ctx->ids_map_b + (size_t)b * V, 0));
+            Hl.ids_host = (long long *)p;
+            CK(cudaHostGetDevicePointer(&p, ctx->logits_map_b + (size_t)b * V, 0));
+            Hl.logits_host = (double *)p;
+            CK(cudaHostGetDevicePointer(&p, ctx->flags_b + b, 0));
+            Hl.host_flag = (volatile unsigned long long *)p;
+            l.Dh = Hl;
+        }
         CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
     }
@@ -465,23 +504,14 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     for (int b = 0; b < B; ++b) {
         Lane &l = ctx->lanes[b];
         CK(cudaStreamWaitEvent(l.stream, ctx->fork, 0));
-        Dev Dl = l.D;
+        Dev Dl = host_io ? l.Dh : l.D;  // host I/O: each lane publishes into mapped memory
         Dl.launch_mode = LAUNCH_STEP;
         void *args[] = {&Dl};
         CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->lane_grid), dim3(THREADS), args, ctx->smem,
                                        l.stream));
-        if (host_io) {
-            const int64_t first = ctx->first_chunk;
-            CK(cudaMemcpyAsync(ctx->ids_pin_b + (size_t)b * first, Dl.S_ids, sizeof(long long) * first,
-                               cudaMemcpyDeviceToHost, l.stream));
-            CK(cudaMemcpyAsync(ctx->logits_pin_b + (size_t)b * first, Dl.S_logits, sizeof(double) * first,
-                               cudaMemcpyDeviceToHost, l.stream));
-        }
         CK(cudaEventRecord(l.done, l.stream));
         CK(cudaStreamWaitEvent(s, l.done, 0));
     }
-    if (host_io)
-        CK(cudaMemcpyAsync(ctx->res_pin_b, ctx->d_res_all, sizeof(csvd_result) * B, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamEndCapture(s, &g));
     CK(cudaGraphInstantiate(&ctx->g_batch, g, 0));
     CK(cudaGraphDestroy(g));
@@ -521,37 +551,62 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
     int rc = batch_prepare(ctx, B, cfg, true);
     if (rc) return rc;
     cudaStream_t s = ctx->stream;
+    static const bool prof = getenv("CSVD_PROFILE_HOST") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
     memcpy(ctx->H_pin, H, sizeof(double) * B * ctx->D.d);
+    const unsigned long long want = ++ctx->batch_seq;
+    auto t1 = now();
     CK(cudaGraphLaunch(ctx->g_batch, s));
-    CK(cudaStreamSynchronize(s));
-    const int64_t first = ctx->first_chunk;
-    int err = 0;
-    for (int b = 0; b < B; ++b) {
-        res[b] = ctx->res_pin_b[b];
-        if (res[b].error && !err) err = b + 1;
+    auto t2 = now();
+    // every lane publishes its result into mapped memory and bumps its flag
+    volatile unsigned long long *flags = ctx->flags_b;
+    int ready = 0;
+    for (unsigned long long spins = 0; ready < B; ++spins) {
+        ready = 0;
+        for (int b = 0; b < B; ++b) ready += flags[b] == want;
+        if (ready < B && (spins & 255) == 255 && cudaStreamQuery(s) != cudaErrorNotReady) {
+            ready = 0;
+            for (int b = 0; b < B; ++b) ready += flags[b] == want;
+            break;
+        }
     }
-    if (err) {
+    if (ready < B) {  // a lane ended without publishing: device error
+        CK(cudaStreamSynchronize(s));
+        std::vector<csvd_result> rr(B);
+        CK(cudaMemcpy(rr.data(), ctx->d_res_all, sizeof(csvd_result) * B, cudaMemcpyDeviceToHost));
+        bool value_err = false;
+        for (auto &r : rr) value_err = value_err || r.error == CSVD_EVALUE;
+        ctx->batch_seq = 0;
+        for (int b = 0; b < B; ++b) ctx->flags_b[b] = 0;
         CK(cudaMemset(ctx->d_res_all, 0, sizeof(csvd_result) * B));
         for (Lane &l : ctx->lanes) {
             CK(cudaMemset(l.D.bar, 0, 16));
             CK(cudaMemset(l.D.cnt, 0, sizeof(int) * ctx->D.C));
+            CK(cudaMemset(l.D.seq, 0, sizeof(unsigned long long)));
+            CK(cudaMemset(l.D.done_ctas, 0, sizeof(unsigned)));
         }
-        const int e = res[err - 1].error;
-        return fail(ctx, e, e == CSVD_EVALUE ? "bounds must be finite" : "device state error (grid barrier timeout)");
+        if (value_err) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
+        return fail(ctx, CSVD_ESTATE, "device state error in a batch lane (grid barrier timeout)");
     }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (prof) {
+        auto t3 = now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        fprintf(stderr, "batch host: stage %.1f us, graph launch %.1f us, wait %.1f us\n", us(t0, t1), us(t1, t2),
+                us(t2, t3));
+    }
+    const int64_t V = ctx->D.V;
     for (int b = 0; b < B; ++b) {
+        memcpy(&res[b], (const void *)(ctx->res_map_b + b), sizeof(csvd_result));
+        if (res[b].error) {
+            const int e = res[b].error;
+            return fail(ctx, e, e == CSVD_EVALUE ? "bounds must be finite" : "device state error");
+        }
         const int64_t n = res[b].sub_size;
         if (n > cap) return fail(ctx, CSVD_EDIM, "output capacity too small");
-        int64_t *ib = ids ? ids + (size_t)b * cap : nullptr;
-        double *lb = logits ? logits + (size_t)b * cap : nullptr;
-        const int64_t m = n < first ? n : first;
-        if (ib) memcpy(ib, ctx->ids_pin_b + (size_t)b * first, sizeof(int64_t) * m);
-        if (lb) memcpy(lb, ctx->logits_pin_b + (size_t)b * first, sizeof(double) * m);
-        if (n > first) {
-            const Dev &L = ctx->lanes[b].D;
-            if (ib) CK(cudaMemcpy(ib + first, L.S_ids + first, sizeof(int64_t) * (n - first), cudaMemcpyDeviceToHost));
-            if (lb) CK(cudaMemcpy(lb + first, L.S_logits + first, sizeof(double) * (n - first), cudaMemcpyDeviceToHost));
-        }
+        if (ids) memcpy(ids + (size_t)b * cap, ctx->ids_map_b + (size_t)b * V, sizeof(int64_t) * n);
+        if (logits) memcpy(logits + (size_t)b * cap, ctx->logits_map_b + (size_t)b * V, sizeof(double) * n);
     }
     return 0;
 }
@@ -910,7 +965,10 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         // zero-copy: the kernel writes ids / logits / result into mapped host
         // memory and raises the flag; spin on it instead of a stream sync
         const unsigned long long want = ++ctx->seq_host;
+        static const bool prof = getenv("CSVD_PROFILE_HOST") != nullptr;
+        auto t1 = std::chrono::steady_clock::now();
         CK(cudaGraphLaunch(ctx->g_host, s));
+        auto t2 = std::chrono::steady_clock::now();
         volatile unsigned long long *flag = ctx->flag_map;
         bool got = false;
         for (unsigned long long spins = 0;; ++spins) {
@@ -925,6 +983,11 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         }
         if (got) {
             std::atomic_thread_fence(std::memory_order_acquire);
+            if (prof) {
+                auto t3 = std::chrono::steady_clock::now();
+                auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+                fprintf(stderr, "step host: graph launch %.1f us, wait %.1f us\n", us(t1, t2), us(t2, t3));
+            }
             memcpy(res, (const void *)ctx->res_map, sizeof(csvd_result));
             if ((rc = result_error(ctx, *res))) return rc;
             const int64_t n = res->sub_size;

@@ -212,15 +212,17 @@ class DeviceIndex:
         B = H.shape[0]
         c = cfg if isinstance(cfg, _lib.Config) else self.make_config(cfg, k_max, variant)
         res = (_lib.Result * B)()
-        ids = np.empty((B, self.V), dtype=np.int64)
-        logits = np.empty((B, self.V), dtype=np.float64)
         with self._lock:
+            if getattr(self, "_bids", None) is None or self._bids.shape[0] < B:  # reused staging
+                self._bids = np.empty((B, self.V), dtype=np.int64)
+                self._blogits = np.empty((B, self.V), dtype=np.float64)
+            ids, logits = self._bids, self._blogits
             self._check(self._lib.csvd_step_batch_host(self._ctx, B, H.ctypes.data, ctypes.byref(c), res,
                                                        ids.ctypes.data, logits.ctypes.data, self.V))
-        out = []
-        for b in range(B):
-            n = int(res[b].sub_size)
-            out.append(self._outcome(res[b], ids[b, :n].copy(), logits[b, :n].copy()))
+            out = []
+            for b in range(B):
+                n = int(res[b].sub_size)
+                out.append(self._outcome(res[b], ids[b, :n].copy(), logits[b, :n].copy()))
         return out
 
     def _outcome(self, r, ids, logits) -> DecodeOutcome:
