@@ -162,8 +162,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(T, ix, q, cfg, seconds):
-    """The oracle port (oracle/csvd_oracle.py) on a bounded sample of the stream."""
+def cpu_baseline(T, ix, q, cfg, seconds, ours=None):
+    """The oracle port (oracle/csvd_oracle.py) on a bounded sample of the stream.
+    Its outcomes double as a full-size parity check of the GPU outcomes of the
+    same queries (token ids, logits bit-exact; certificate and fallback)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import csvd_oracle as O
     O.set_threads(0)
@@ -171,16 +173,27 @@ def cpu_baseline(T, ix, q, cfg, seconds):
     O.decode_step(T, ix, q[0], cfg)  # warm (builds nothing, touches pages)
     n, t0 = 0, time.perf_counter()
     fb = 0
+    refs = []
     while n < len(q) and (time.perf_counter() - t0) < seconds:
         out = O.decode_step(T, ix, q[n], cfg)
         fb += out.fallback_used is not None
+        refs.append(out)
         n += 1
     dt = time.perf_counter() - t0
+    parity = None
+    if ours is not None:
+        m = min(len(ours), len(refs))
+        bad = sum(not (np.array_equal(o.token_ids, r.token_ids) and np.array_equal(o.logits, r.logits)
+                       and o.status.kind == r.status.kind and o.fallback_used == r.fallback_used
+                       and o.status.topk_min == r.status.topk_min)
+                  for o, r in zip(ours[:m], refs[:m]))
+        parity = {"steps_checked": m, "mismatches": int(bad),
+                  "checks": "token ids + f64 logits bit-exact, kind, fallback, k-th logit"}
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{n} consecutive steps of the same contextual query stream ({dt:.1f} s), "
                       f"oracle/csvd_oracle.py decode_step with the per-step SHA-256 fingerprint of the "
                       f"reference memoized and the pairwise f64 GEMV in C on {cores} threads",
-            "fallback_rate": fb / max(n, 1)}
+            "fallback_rate": fb / max(n, 1), "parity_vs_gpu": parity}
 
 
 C3 = dict(V=151552, d=3584, C=2273, g=1, dtype="bf16", B=16, eps=1e-3)
@@ -474,7 +487,7 @@ def run_ours(a):
     if sharded is not None:
         line["sharded"] = sharded
     if not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(T, ix, q[W:], cfg, a.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(T, ix, q[W:], cfg, a.cpu_seconds, ours=outs)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
