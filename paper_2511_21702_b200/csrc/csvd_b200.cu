@@ -67,6 +67,9 @@ struct csvd_ctx {
     std::vector<void *> dev_allocs;
     void *k_buffers[4] = {};  // K-dependent: dense candidate lists, cluster top-k summaries
     kern_t kern = nullptr;
+    kern_t kdense = nullptr;  // standalone full-vocabulary GEMV (regular plans)
+    int dense_grid = 0;
+    size_t dense_smem = 0;
     int grid = 0;
     int nsm = 0;
     size_t smem = 0;
@@ -197,7 +200,8 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
 // (instantiated in kinst.cu, one translation unit per dtype / plan)
 #define CSVD_EXTERN_K(ET, CPL, Q)                                  \
     extern template __global__ void k_step<ET, CPL, Q, CPL, Q>(Dev); \
-    extern template __global__ void k_step<ET, CPL, Q, 0, 0>(Dev);
+    extern template __global__ void k_step<ET, CPL, Q, 0, 0>(Dev);   \
+    extern template __global__ void k_dense_gemv<ET, CPL, Q>(Dev);
 #define CSVD_EXTERN_ET(ET) \
     CSVD_EXTERN_K(ET, 8, 1) CSVD_EXTERN_K(ET, 8, 2) CSVD_EXTERN_K(ET, 8, 4) \
     CSVD_EXTERN_K(ET, 4, 1) CSVD_EXTERN_K(ET, 2, 1) CSVD_EXTERN_K(ET, 1, 1)
@@ -222,6 +226,21 @@ static kern_t pick_w(const PwPlan &wp, const PwPlan &bp) {
         case 2 * 8 + 1: return pick_b<ET, 2, 1>(same);
         default: return pick_b<ET, 1, 1>(same);
     }
+}
+template <typename ET>
+static kern_t pick_dense_t(const PwPlan &wp) {
+    if (!wp.regular) return nullptr;
+    switch (wp.cpl * 8 + wp.q) {
+        case 8 * 8 + 1: return k_dense_gemv<ET, 8, 1>;
+        case 8 * 8 + 2: return k_dense_gemv<ET, 8, 2>;
+        case 8 * 8 + 4: return k_dense_gemv<ET, 8, 4>;
+        case 4 * 8 + 1: return k_dense_gemv<ET, 4, 1>;
+        case 2 * 8 + 1: return k_dense_gemv<ET, 2, 1>;
+        default: return k_dense_gemv<ET, 1, 1>;
+    }
+}
+static kern_t pick_dense(const Dev &D) {
+    return D.wdtype == CSVD_W_BF16 ? pick_dense_t<uint16_t>(D.wplan) : pick_dense_t<float>(D.wplan);
 }
 static kern_t pick_kernel(const Dev &D) {
     return D.wdtype == CSVD_W_BF16 ? pick_w<uint16_t>(D.wplan, D.bplan) : pick_w<float>(D.wplan, D.bplan);
@@ -288,6 +307,16 @@ static int configure(csvd_ctx *ctx) {
     if (occ < 1) return fail(ctx, CSVD_ECONFIG, "step kernel does not fit on an SM");
     ctx->grid = ctx->nsm * occ;
     D.nblocks = ctx->grid;
+    ctx->kdense = getenv("CSVD_DENSE_PERSISTENT") ? nullptr : pick_dense(D);
+    D.dense_pd = getenv("CSVD_DENSE_PD") ? atoi(getenv("CSVD_DENSE_PD")) : 1;
+    if (ctx->kdense) {
+        ctx->dense_smem = sizeof(double) * (size_t)pw_hs_size(D.wplan);
+        CK(cudaFuncSetAttribute((const void *)ctx->kdense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ctx->dense_smem));
+        int occ2 = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ctx->kdense, THREADS, ctx->dense_smem));
+        ctx->dense_grid = ctx->nsm * (occ2 > 0 ? occ2 : 1);
+    }
     if ((long long)D.C > (long long)MAX_PER_WARP * ctx->grid * WARPS)
         return fail(ctx, CSVD_ECONFIG, "too many clusters for the resident grid");
     return 0;
@@ -296,6 +325,11 @@ static int configure(csvd_ctx *ctx) {
 static int launch(csvd_ctx *ctx, int mode, cudaStream_t s, bool host_map = false) {
     Dev D = host_map ? ctx->Dhost : ctx->D;
     D.launch_mode = mode;
+    if (mode == LAUNCH_DENSE && ctx->kdense && !ctx->shard) {  // standalone GEMV: no k-th / top-k needed
+        ctx->kdense<<<ctx->dense_grid, THREADS, ctx->dense_smem, s>>>(D);
+        CK(cudaGetLastError());
+        return 0;
+    }
     void *args[] = {&D};
     CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->grid), dim3(THREADS), args, ctx->smem, s));
     return 0;

@@ -87,6 +87,7 @@ struct Dev {
     int nblocks;
     int launch_mode;
     int pre_bounds;          // 1: Uraw / dots / query_norm come from k_bounds_batch
+    int dense_pd;            // k_dense_gemv: rows prefetched ahead per warp
     int hs_off_b;            // offset (doubles) of the bounds h layout, 0 = shared with W
     int scratch_off;         // generic-path per-warp leaf scratch
     int ord_off;             // ordering arrays (rank staging, then order/cum/Uo/lrh)
@@ -1724,5 +1725,38 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// standalone full-vocabulary GEMV (oracle.dense_logits, oracle.py:33-41): the
+// same exact row dot as the step's fallback, as its own high-occupancy kernel
+// (2 CTAs / 16 warps per SM, <= 128 registers) so more rows are in flight;
+// logits scattered to token order.  Regular plans only.
+// ---------------------------------------------------------------------------
+template <typename ET, int CPL, int Q>
+__global__ void __launch_bounds__(THREADS, 2) k_dense_gemv(Dev D) {
+    extern __shared__ __align__(16) double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pw_stage<CPL>(D.wplan, D.h, D.d, smem, D.wsrc);
+    __syncthreads();
+    const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
+    const int PD = D.dense_pd;  // rows kept in flight ahead through L2 bulk prefetches
+    const size_t rb = (size_t)D.d * sizeof(ET);
+    if (lane == 0)
+        for (int j = 0; j < PD; ++j) {
+            const int r = gwarp + j * nwarps;
+            if (r < D.Vl) bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)r * rb, rb);
+        }
+    for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
+        if (PD > 0 && lane == 0 && lr + PD * nwarps < D.Vl)
+            bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(lr + PD * nwarps) * rb, rb);
+        const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
+        const double logit = row_logit<ET, CPL, Q>(D, lr, pos, smem, nullptr, lane);
+        if (lane == 0) {
+            const int tok = __ldg(D.perm + pos);
+            D.S_logits[tok] = logit;
+            D.S_ids[tok] = tok;
+        }
     }
 }

@@ -7,3 +7,6 @@
 template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q>(Dev);
 #endif
 template __global__ void k_step<KI_ET, KI_CPL, KI_Q, 0, 0>(Dev);
+#if KI_CPL > 0
+template __global__ void k_dense_gemv<KI_ET, KI_CPL, KI_Q>(Dev);
+#endif
