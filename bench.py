@@ -479,7 +479,9 @@ def run_ours(a):
                        "achieved_gbs": dense_bytes / (dense_mean * 1e-3) / 1e9,
                        "frac": dense_bytes / (dense_mean * 1e-3) / 1e9 / pk},
         "speedup_vs_dense_gemv": dense_mean / mean_ms,
-        "gpu_launches": int(sum(1 + w for w in waves)),
+        # timed region: one persistent k_step per step (whatever its waves) plus
+        # the L2-flush kernel before each step
+        "gpu_launches": K * (1 if a.no_flush else 2),
         "clocks": clk.summary(),
     }
     if batched is not None:
