@@ -469,7 +469,7 @@ def run_ours(a):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
                      "traffic": traffic, "peak_kind": pk_kind,
-                     "kernel": "whole step (k_bounds + k_wave graph)",
+                     "kernel": "k_step (one persistent cooperative launch per step; bounds, head, rows, certification)",
                      "algorithmic_bytes_per_step": mean_bytes},
         "fallback_rate": fallbacks / K,
         "mean_sub_ratio": float(np.mean([o.stats.ratio for o in outs])),

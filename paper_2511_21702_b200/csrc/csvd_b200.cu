@@ -309,7 +309,10 @@ static int configure(csvd_ctx *ctx) {
     ctx->grid = ctx->nsm * occ;
     D.nblocks = ctx->grid;
     ctx->kdense = getenv("CSVD_DENSE_PERSISTENT") ? nullptr : pick_dense(D);
-    D.dense_pd = getenv("CSVD_DENSE_PD") ? atoi(getenv("CSVD_DENSE_PD")) : 1;
+    // L2 bulk prefetch policy (measured: prefetching rows ahead in the dense GEMV
+    // causes re-reads and costs 25%; CSVD_DENSE_PD / CSVD_PF override)
+    D.dense_pd = getenv("CSVD_DENSE_PD") ? atoi(getenv("CSVD_DENSE_PD")) : 0;
+    D.pf_mask = getenv("CSVD_PF") ? atoi(getenv("CSVD_PF")) : 0;  // step: no measurable gain either way
     if (ctx->kdense) {
         ctx->dense_smem = sizeof(double) * (size_t)pw_hs_size(D.wplan);
         CK(cudaFuncSetAttribute((const void *)ctx->kdense, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -88,6 +88,7 @@ struct Dev {
     int launch_mode;
     int pre_bounds;          // 1: Uraw / dots / query_norm come from k_bounds_batch
     int dense_pd;            // k_dense_gemv: rows prefetched ahead per warp
+    int pf_mask;             // L2 bulk prefetch: 1 centroid rows + per-cluster arrays, 2 wave rows
     int hs_off_b;            // offset (doubles) of the bounds h layout, 0 = shared with W
     int scratch_off;         // generic-path per-warp leaf scratch
     int ord_off;             // ordering arrays (rank staging, then order/cum/Uo/lrh)
@@ -1176,7 +1177,7 @@ __device__ void wave_rows(const Dev &D, const Ord &o, int p_lo, int p_hi, const 
     const int row_lo = o.cum[p_lo], row_hi = o.cum[p_hi];
     const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
     const size_t rb = (size_t)D.d * sizeof(ET);
-    if (lane == 0) {  // every row of this warp in flight at once (L2 prefetch)
+    if ((D.pf_mask & 2) && lane == 0) {  // every row of this warp in flight at once (L2 prefetch)
         for (int r = row_lo + gwarp; r < row_hi; r += nwarps) {
             int lo = p_lo, hi = p_hi;
             while (hi - lo > 1) {
@@ -1220,9 +1221,9 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
     double lv = -INFINITY;  // small k: lane l holds the l-th largest so far
     int cnt = 0;
     double kmin = -INFINITY;
-    // rows stream through L2: lane 0 keeps the warp's next PD rows in flight
-    // with bulk prefetches, so HBM sees ~PD x 1184 rows of requests at all times
-    constexpr int PD = 2;
+    // optional L2 bulk prefetch of the warp's next rows (off by default: it was
+    // measured to cause re-reads, 2.6 GB of DRAM traffic for 2.1 GB of rows)
+    const int PD = D.dense_pd;
     const size_t rb = (size_t)D.d * sizeof(ET);
     if (lane == 0)
         for (int j = 0; j < PD; ++j) {
@@ -1231,7 +1232,7 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
         }
     for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
         const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
-        if (lane == 0 && lr + PD * nwarps < D.Vl)
+        if (PD > 0 && lane == 0 && lr + PD * nwarps < D.Vl)
             bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(lr + PD * nwarps) * rb, rb);
         const double logit = row_logit<ET, CPL, Q>(D, lr, pos, hs, scratch, lane);
         if (lane == 0) {
@@ -1541,7 +1542,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
     if (D.launch_mode != LAUNCH_BOUNDS) pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
     if (!D.pre_bounds && (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b))
         pw_stage<BCPL>(D.bplan, D.h, D.d, hs_b, D.bsrc);
-    if (D.launch_mode != LAUNCH_DENSE && !D.pre_bounds && lane == 0) {
+    if (D.launch_mode != LAUNCH_DENSE && !D.pre_bounds && (D.pf_mask & 1) && lane == 0) {
         // start the HBM reads of this warp's centroid rows (and, in CTA 0, the
         // per-cluster arrays every CTA reads later) while h is staged
         const int c = warp * gridDim.x + blockIdx.x;
