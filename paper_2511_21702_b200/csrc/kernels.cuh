@@ -1710,7 +1710,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
     __syncthreads();
     const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
-    if (lane == 0)  // this warp's centroid rows start streaming into L2 (later passes hit there)
+    if ((D.pf_mask & 1) && lane == 0)  // optional: this warp's centroid rows towards L2
         for (int c = gwarp; c < D.C; c += nwarps) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
     for (int qb = 0; qb < B; qb += BQN) {
         const int nq = min(BQN, B - qb);
