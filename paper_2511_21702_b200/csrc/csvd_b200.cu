@@ -113,6 +113,8 @@ struct csvd_ctx {
     double *logits_pin_b = nullptr;
     cudaEvent_t fork = nullptr;
     double **d_Uraw_l = nullptr, **d_dots_l = nullptr;  // [lanes] per-lane bound outputs
+    kern_t kgroup = nullptr;                      // grouped lanes kernel (one launch per batch)
+    LaneWS *d_lanes = nullptr, *d_lanes_host = nullptr;
     void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *) = nullptr;
     size_t kbb_smem = 0;
     cudaGraphExec_t g_batch = nullptr;
@@ -202,7 +204,8 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
 #define CSVD_EXTERN_K(ET, CPL, Q)                                  \
     extern template __global__ void k_step<ET, CPL, Q, CPL, Q>(Dev); \
     extern template __global__ void k_step<ET, CPL, Q, 0, 0>(Dev);   \
-    extern template __global__ void k_dense_gemv<ET, CPL, Q>(Dev);
+    extern template __global__ void k_dense_gemv<ET, CPL, Q>(Dev);   \
+    extern template __global__ void k_step<ET, CPL, Q, CPL, Q, true>(Dev);
 #define CSVD_EXTERN_ET(ET) \
     CSVD_EXTERN_K(ET, 8, 1) CSVD_EXTERN_K(ET, 8, 2) CSVD_EXTERN_K(ET, 8, 4) \
     CSVD_EXTERN_K(ET, 4, 1) CSVD_EXTERN_K(ET, 2, 1) CSVD_EXTERN_K(ET, 1, 1)
@@ -242,6 +245,22 @@ static kern_t pick_dense_t(const PwPlan &wp) {
 }
 static kern_t pick_dense(const Dev &D) {
     return D.wdtype == CSVD_W_BF16 ? pick_dense_t<uint16_t>(D.wplan) : pick_dense_t<float>(D.wplan);
+}
+template <typename ET>
+static kern_t pick_grouped_t(const PwPlan &wp, const PwPlan &bp) {
+    if (!wp.regular || wp.n != bp.n) return nullptr;
+    switch (wp.cpl * 8 + wp.q) {
+        case 8 * 8 + 1: return k_step<ET, 8, 1, 8, 1, true>;
+        case 8 * 8 + 2: return k_step<ET, 8, 2, 8, 2, true>;
+        case 8 * 8 + 4: return k_step<ET, 8, 4, 8, 4, true>;
+        case 4 * 8 + 1: return k_step<ET, 4, 1, 4, 1, true>;
+        case 2 * 8 + 1: return k_step<ET, 2, 1, 2, 1, true>;
+        default: return k_step<ET, 1, 1, 1, 1, true>;
+    }
+}
+static kern_t pick_grouped(const Dev &D) {
+    return D.wdtype == CSVD_W_BF16 ? pick_grouped_t<uint16_t>(D.wplan, D.bplan)
+                                   : pick_grouped_t<float>(D.wplan, D.bplan);
 }
 static kern_t pick_kernel(const Dev &D) {
     return D.wdtype == CSVD_W_BF16 ? pick_w<uint16_t>(D.wplan, D.bplan) : pick_w<float>(D.wplan, D.bplan);
@@ -517,6 +536,52 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaFuncSetAttribute((const void *)ctx->kbb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ctx->kbb_smem));
     }
+    {  // per-lane workspace tables for the grouped launch
+        auto ws = [](const Dev &L) {
+            LaneWS w{};
+            w.h = L.h;
+            w.U = L.U;
+            w.Uraw = L.Uraw;
+            w.dots = L.dots;
+            w.cnt = L.cnt;
+            w.order_g = L.order_g;
+            w.cum_g = L.cum_g;
+            w.sum_lse = L.sum_lse;
+            w.sum_min = L.sum_min;
+            w.sum_max = L.sum_max;
+            w.S_logits = L.S_logits;
+            w.S_ids = L.S_ids;
+            w.st = L.st;
+            w.res = L.res;
+            w.bar = L.bar;
+            w.cand = L.cand;
+            w.sum_topk = L.sum_topk;
+            w.shard_out = L.shard_out;
+            w.res_host = L.res_host;
+            w.ids_host = L.ids_host;
+            w.logits_host = L.logits_host;
+            w.host_flag = L.host_flag;
+            w.done_ctas = L.done_ctas;
+            w.seq = L.seq;
+            return w;
+        };
+        std::vector<LaneWS> td(B), th(B);
+        for (int b = 0; b < B; ++b) {
+            td[b] = ws(ctx->lanes[b].D);
+            th[b] = ws(ctx->lanes[b].Dh);
+        }
+        if ((rc = lalloc(ctx, &ctx->d_lanes, B)) || (rc = lalloc(ctx, &ctx->d_lanes_host, B))) return rc;
+        CK(cudaMemcpy(ctx->d_lanes, td.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_lanes_host, th.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
+        ctx->kgroup = (getenv("CSVD_LANES_FORKED") || B * G > ctx->grid) ? nullptr : pick_grouped(D0);
+        if (ctx->kgroup) {
+            CK(cudaFuncSetAttribute((const void *)ctx->kgroup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ctx->smem));
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kgroup, THREADS, ctx->smem));
+            if (occ * ctx->nsm < B * G) ctx->kgroup = nullptr;
+        }
+    }
     ctx->lane_grid = G;
     ctx->lane_K = K;
     ctx->lane_plain = getenv("CSVD_LANE_PLAIN") && atoi(getenv("CSVD_LANE_PLAIN")) > 0 && B * G <= ctx->nsm;
@@ -531,13 +596,27 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     cudaGraph_t g;
     const Dev &D0 = ctx->D;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    if (host_io)
+    if (host_io && !getenv("CSVD_BATCH_H_OUTSIDE"))
         CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
         ctx->kbb<<<ctx->grid, THREADS, ctx->kbb_smem, s>>>(D0, ctx->d_H, B, ctx->d_Uraw_l, ctx->d_dots_l,
                                                            ctx->d_res_all);
         CK(cudaGetLastError());
+    }
+    if (ctx->kgroup) {  // every lane in one cooperative launch of B x G CTAs
+        Dev Dg = host_io ? ctx->lanes[0].Dh : ctx->lanes[0].D;
+        Dg.launch_mode = LAUNCH_STEP;
+        Dg.lanes = host_io ? ctx->d_lanes_host : ctx->d_lanes;
+        void *args[] = {&Dg};
+        CK(cudaLaunchCooperativeKernel((const void *)ctx->kgroup, dim3(B * ctx->lane_grid), dim3(THREADS), args,
+                                       ctx->smem, s));
+        CK(cudaStreamEndCapture(s, &g));
+        CK(cudaGraphInstantiate(&ctx->g_batch, g, 0));
+        CK(cudaGraphDestroy(g));
+        ctx->g_batch_B = B;
+        ctx->g_batch_host = host_io ? 1 : 0;
+        return 0;
     }
     CK(cudaEventRecord(ctx->fork, s));
     for (int b = 0; b < B; ++b) {
@@ -603,10 +682,14 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
     auto t0 = now();
     memcpy(ctx->H_pin, H, sizeof(double) * B * ctx->D.d);
     const unsigned long long want = ++ctx->batch_seq;
+    static const bool h_outside = getenv("CSVD_BATCH_H_OUTSIDE") != nullptr;
+    if (h_outside) CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * ctx->D.d, cudaMemcpyHostToDevice, s));
     auto t1 = now();
     CK(cudaGraphLaunch(ctx->g_batch, s));
     auto t2 = now();
     // every lane publishes its result into mapped memory and bumps its flag
+    static const bool sync_wait = getenv("CSVD_BATCH_SYNC") != nullptr;
+    if (sync_wait) CK(cudaStreamSynchronize(s));
     volatile unsigned long long *flags = ctx->flags_b;
     int ready = 0;
     for (unsigned long long spins = 0; ready < B; ++spins) {
@@ -873,6 +956,7 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     CK(cudaMemset(D.res, 0, sizeof(csvd_result)));
     D.dbg = nullptr;
     D.pre_bounds = 0;
+    D.lanes = nullptr;
     if (getenv("CSVD_DEBUG_TS") && atoi(getenv("CSVD_DEBUG_TS")) > 0) {
         if ((rc = dalloc(ctx, &D.dbg, 128))) return rc;
         CK(cudaMemset(D.dbg, 0, 128 * 8));

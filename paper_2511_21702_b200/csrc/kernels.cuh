@@ -44,6 +44,26 @@
 
 enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2, LAUNCH_SHARD = 3 };
 
+// Per-step workspace of one batch lane (grouped launches: lane b's CTAs are
+// blockIdx.x in [b*G, (b+1)*G) and swap these pointers into their Dev).
+struct LaneWS {
+    const double *h;
+    double *U, *Uraw, *dots;
+    int *cnt, *order_g, *cum_g;
+    double *sum_lse, *sum_min, *sum_max, *S_logits;
+    long long *S_ids;
+    ScanState *st;
+    csvd_result *res;
+    unsigned *bar;
+    double *cand, *sum_topk, *shard_out;
+    csvd_result *res_host;
+    long long *ids_host;
+    double *logits_host;
+    volatile unsigned long long *host_flag;
+    unsigned *done_ctas;
+    unsigned long long *seq;
+};
+
 struct Dev {
     int V, d, C, Cp, bd, mode, wdtype;  // Cp: C rounded up to a power of two (sort)
     int K;  // top-k capacity (row stride of the dense candidate lists, list buffers)
@@ -89,6 +109,7 @@ struct Dev {
     int pre_bounds;          // 1: Uraw / dots / query_norm come from k_bounds_batch
     int dense_pd;            // k_dense_gemv: rows prefetched ahead per warp
     int pf_mask;             // L2 bulk prefetch: 1 centroid rows + per-cluster arrays, 2 wave rows
+    const LaneWS *lanes;     // grouped batch launch: per-lane workspaces (null otherwise)
     int hs_off_b;            // offset (doubles) of the bounds h layout, 0 = shared with W
     int scratch_off;         // generic-path per-warp leaf scratch
     int ord_off;             // ordering arrays (rank staging, then order/cum/Uo/lrh)
@@ -96,6 +117,11 @@ struct Dev {
     int chunk;               // clusters per summary/scan chunk (<= CHUNK)
     unsigned long long *dbg; // optional phase timestamps (CSVD_DEBUG_TS)
 };
+
+// this CTA's index / the CTA count of its step's grid: the whole launch, or
+// one batch lane's group of D.nblocks CTAs in a grouped launch
+#define CTA_ID ((int)(blockIdx.x % (unsigned)D.nblocks))
+#define CTA_N (D.nblocks)
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -329,7 +355,7 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ double s_qn;
     __shared__ double s_dot[WARPS][MAX_PER_WARP];
-    const int stride = gridDim.x * WARPS;
+    const int stride = CTA_N * WARPS;
     if (warp == 0) {  // ||h|| = sqrt(sum(h*h)) in the pairwise order (_linalg.py:40-43)
         double ss;
         if constexpr (BCPL > 0) {
@@ -344,7 +370,7 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
         if (lane == 0) s_qn = __dsqrt_rn(ss);
     }
     int j = 0;
-    for (int c = warp * gridDim.x + blockIdx.x; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
+    for (int c = warp * CTA_N + CTA_ID; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
         double dot = warp_dot_t<double, BCPL, BQ>(D.cent + (size_t)c * D.bd, hs, D.bplan, scratch, lane);
         if (lane == 0) s_dot[warp][j] = dot;
     }
@@ -352,7 +378,7 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
     const double qn = s_qn;
     if (lane == 0) {
         j = 0;
-        for (int c = warp * gridDim.x + blockIdx.x; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
+        for (int c = warp * CTA_N + CTA_ID; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
             const double dot = s_dot[warp][j];
             double u;
             if (D.mode == CSVD_MODE_SPHERICAL)
@@ -365,7 +391,7 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
             D.dots[c] = dot;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) D.res->query_norm = qn;
+    if (CTA_ID == 0 && threadIdx.x == 0) D.res->query_norm = qn;
 }
 
 // ---------------------------------------------------------------------------
@@ -457,10 +483,10 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, 
         bad |= !isfinite(u);  // BoundVector.__post_init__ (bounds.py:53-55)
         Us[c] = u;
         xs[c] = __dadd_rn(xs[c], u);  // certify.py:119 np.log(sizes) + U
-        if (blockIdx.x == 0) D.U[c] = u;
+        if (CTA_ID == 0) D.U[c] = u;
     }
     bad = __syncthreads_or(bad);
-    if (blockIdx.x == 0 && tid == 0) D.res->slack = eta;
+    if (CTA_ID == 0 && tid == 0) D.res->slack = eta;
     return !bad;
 }
 
@@ -847,10 +873,10 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
             mn = fmin(mn, x);
         }
     }
-    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 48);
+    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 48);
     mx = warp_max(mx);
     mn = warp_min(mn);
-    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 49);
+    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 49);
     double s = 0.0;
     if (in_regs) {
 #pragma unroll
@@ -860,7 +886,7 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
         for (int i = lane; i < n; i += 32) s = __dadd_rn(s, csvd_exp(__dsub_rn(__ldcg(v + i), mx)));
     }
     s = warp_sum(s);
-    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 50);
+    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 50);
     if (in_regs) {
         // top-kk values (only the values matter: the list holds no ids).
         // Each lane sorts its 8 values (Batcher network), then kk rounds of a
@@ -880,7 +906,7 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
         CSVD_CAS(2, 4) CSVD_CAS(3, 5)
         CSVD_CAS(3, 4)
 #undef CSVD_CAS
-    if (D.dbg && blockIdx.x == 0 && threadIdx.x == 0) DBG_TS(D, 51);
+    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 51);
 #pragma unroll 1
         for (int j = 0; j < kk; ++j) {
             const unsigned long long key = dkey(reg[0]);
@@ -1025,7 +1051,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
         pmn = fmin(pmn, st0.smin);
         pmx = fmax(pmx, st0.smax);
     }
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 40);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 40);
     // streaming log Z_S (certify.py:83 logaddexp chain) as a prefix sum of
     // exp(lse - M) over the chunk, M the chunk's largest term (incl. the carry)
     double lz;
@@ -1044,7 +1070,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             lz = t > 0.0 ? __dadd_rn(M, csvd_log(t)) : -INFINITY;
         }
     }
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 41);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 41);
     // the reference recomputes log Z_S over all of S when the merge count p % 64 == 0
     const int rlane = (q0 / 64) * 64 + 63 - q0;
     if (rlane < q1 - q0) {
@@ -1067,7 +1093,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
         if (lane == rlane) lz = full;
         if (lane > rlane) lz = (mm == -INFINITY) ? -INFINITY : __dadd_rn(mm, csvd_log(sv));
     }
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 42);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 42);
     // k-th largest after each merge (exact)
     double my_kth = -INFINITY;
     int kc = ss.kcount;
@@ -1110,7 +1136,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             __syncwarp();
         }
     }
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 43);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 43);
     double *c_lz = c_vals, *c_kth = c_vals + CHUNK, *c_mn = c_vals + 2 * CHUNK, *c_mx = c_vals + 3 * CHUNK;
     double *c_rho = c_vals + 4 * CHUNK, *c_dl = c_vals + 5 * CHUNK;
     if (act) {
@@ -1128,7 +1154,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
     ScanState stl = st0;
     Scan sc{in, stl, res};
     const csvd_config &cfg = *D.cfg;
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 44);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 44);
     if (stl.phase == PH_MAIN && cfg.variant == CSVD_VARIANT_INCREMENTAL) {
         // Common path, all prefixes of the chunk at once: the first prefix that
         // trips the budget (decode.py:342) or passes a target (decode.py:192-210).
@@ -1156,9 +1182,9 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             stl.heap_pops = stl.p;
         }
     }
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 45);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 45);
     sc.run(chk);
-    if (blockIdx.x == 0 && lane == 0) DBG_TS(D, 46);
+    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 46);
     __syncwarp();
     if (lane == 0) {
         ss.st = stl;
@@ -1175,7 +1201,7 @@ template <typename ET, int CPL, int Q>
 __device__ void wave_rows(const Dev &D, const Ord &o, int p_lo, int p_hi, const double *hs, double *scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int row_lo = o.cum[p_lo], row_hi = o.cum[p_hi];
-    const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
+    const int gwarp = CTA_ID * WARPS + warp, nwarps = CTA_N * WARPS;
     const size_t rb = (size_t)D.d * sizeof(ET);
     if ((D.pf_mask & 2) && lane == 0) {  // every row of this warp in flight at once (L2 prefetch)
         for (int r = row_lo + gwarp; r < row_hi; r += nwarps) {
@@ -1214,7 +1240,7 @@ __device__ void wave_rows(const Dev &D, const Ord &o, int p_lo, int p_hi, const 
 template <typename ET, int CPL, int Q>
 __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
+    const int gwarp = CTA_ID * WARPS + warp, nwarps = CTA_N * WARPS;
     const int k = D.cfg->k;
     double *mylist = D.cand + (size_t)gwarp * D.K;
     const bool small_k = k <= 32;
@@ -1354,8 +1380,8 @@ __device__ __forceinline__ bool head_eligible(const csvd_config &cfg) {
 // sequence number the host is spinning on.
 static __device__ __noinline__ void publish_host(const Dev &D, long long n, const csvd_result *r_cta0) {
     if (!D.res_host) return;
-    const long long per = (n + gridDim.x - 1) / gridDim.x;
-    const long long a = (long long)blockIdx.x * per, b = min(n, a + per);
+    const long long per = (n + CTA_N - 1) / CTA_N;
+    const long long a = (long long)CTA_ID * per, b = min(n, a + per);
     for (long long i = a + threadIdx.x; i < b; i += THREADS) {
         D.ids_host[i] = __ldcg(D.S_ids + i);
         D.logits_host[i] = __ldcg(D.S_logits + i);
@@ -1365,7 +1391,7 @@ static __device__ __noinline__ void publish_host(const Dev &D, long long n, cons
         if (r_cta0) *D.res_host = *r_cta0;
         __threadfence_system();
         const unsigned t = atomicAdd(D.done_ctas, 1u);
-        if (t == gridDim.x - 1) {
+        if (t == CTA_N - 1) {
             *D.done_ctas = 0;
             const unsigned long long sq = *D.seq + 1;
             *D.seq = sq;
@@ -1390,7 +1416,7 @@ static __device__ __forceinline__ void next_wave(const Dev &D, const Ord &o, Sca
         s2.wave_tokens = s2.wave_tokens * 2 < D.V ? s2.wave_tokens * 2 : (int)D.V;
     }
     ss.st = s2;
-    if (s2.phase == PH_DONE && blockIdx.x == 0) {
+    if (s2.phase == PH_DONE && CTA_ID == 0) {
         csvd_result r = ss.res;
         r.query_norm = D.res->query_norm;
         r.slack = D.res->slack;
@@ -1418,7 +1444,7 @@ __device__ void shard_open(const Dev &D, const Ord &o, ScanShared &ss, const dou
     const int p_hi = max(p_lo, min(cfg.shard_hi > 0 ? cfg.shard_hi : ss.st.p_sel, C));
     wave_rows<ET, CPL, Q>(D, o, p_lo, p_hi, hs, scratch);
     grid_sync(D);
-    if (blockIdx.x != 0) return;
+    if (CTA_ID != 0) return;
     double *c_lse = sws, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
     double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
     __shared__ int s_own[CHUNK];
@@ -1518,7 +1544,7 @@ static __device__ __noinline__ void lane_query_norm(const Dev &D, const double *
         const double qn = __dsqrt_rn(warp_selfdot_smem<BQ>(hs, D.bplan.leaf_len, lane));
         if (lane == 0) {
             out = qn;
-            if (blockIdx.x == 0) D.res->query_norm = qn;
+            if (CTA_ID == 0) D.res->query_norm = qn;
         }
     }
     __syncthreads();
@@ -1528,8 +1554,7 @@ static __device__ __noinline__ void lane_query_norm(const Dev &D, const double *
 // the step kernel
 // ---------------------------------------------------------------------------
 template <typename ET, int CPL, int Q, int BCPL, int BQ>
-__global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
-    extern __shared__ __align__(16) double smem[];
+__device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *hs_w = smem;
     double *hs_b = D.hs_off_b ? smem + D.hs_off_b : smem;
@@ -1537,7 +1562,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
     double *ws = smem + D.ord_off;
     double *sws = smem + D.sum_off;
     __shared__ ScanShared ss;
-    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool lead = CTA_ID == 0 && threadIdx.x == 0;
     if (lead) DBG_TS(D, 0);
     if (D.launch_mode != LAUNCH_BOUNDS) pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
     if (!D.pre_bounds && (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b))
@@ -1545,9 +1570,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
     if (D.launch_mode != LAUNCH_DENSE && !D.pre_bounds && (D.pf_mask & 1) && lane == 0) {
         // start the HBM reads of this warp's centroid rows (and, in CTA 0, the
         // per-cluster arrays every CTA reads later) while h is staged
-        const int c = warp * gridDim.x + blockIdx.x;
+        const int c = warp * CTA_N + CTA_ID;
         if (c < D.C) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
-        if (blockIdx.x == 0 && warp == WARPS - 1) {
+        if (CTA_ID == 0 && warp == WARPS - 1) {
             bulk_prefetch_l2(D.logsz, sizeof(double) * D.C);
             bulk_prefetch_l2(D.sizes, sizeof(int) * D.C);
             bulk_prefetch_l2(D.meanb, sizeof(double) * D.C);
@@ -1657,13 +1682,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
                 r.slack = D.res->slack;
                 r.waves = ss.st.iter;
                 r.error = __ldcg(&D.res->error);
-                publish_host(D, r.sub_size, blockIdx.x == 0 ? &r : nullptr);
+                publish_host(D, r.sub_size, CTA_ID == 0 ? &r : nullptr);
             }
             if (lead) DBG_TS(D, 11 + 4 * (st.iter & 3));
         } else {  // MODE_DENSE
             dense_rows<ET, CPL, Q>(D, hs_w, scratch);
             grid_sync(D);
-            if (blockIdx.x != 0) {
+            if (CTA_ID != 0) {
                 publish_host(D, D.V, nullptr);
                 break;
             }
@@ -1689,6 +1714,43 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D) {
             publish_host(D, D.V, &ss.res);
             break;
         }
+    }
+}
+
+template <typename ET, int CPL, int Q, int BCPL, int BQ, bool GROUPED = false>
+__global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
+    if constexpr (GROUPED) {
+        // one launch runs a whole batch: lane b is blockIdx.x / nblocks and
+        // swaps its own workspaces into the Dev (all table data is shared)
+        Dev D = D0;
+        const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
+        D.h = w.h;
+        D.U = w.U;
+        D.Uraw = w.Uraw;
+        D.dots = w.dots;
+        D.cnt = w.cnt;
+        D.order_g = w.order_g;
+        D.cum_g = w.cum_g;
+        D.sum_lse = w.sum_lse;
+        D.sum_min = w.sum_min;
+        D.sum_max = w.sum_max;
+        D.S_logits = w.S_logits;
+        D.S_ids = w.S_ids;
+        D.st = w.st;
+        D.res = w.res;
+        D.bar = w.bar;
+        D.cand = w.cand;
+        D.sum_topk = w.sum_topk;
+        D.shard_out = w.shard_out;
+        D.res_host = w.res_host;
+        D.ids_host = w.ids_host;
+        D.logits_host = w.logits_host;
+        D.host_flag = w.host_flag;
+        D.done_ctas = w.done_ctas;
+        D.seq = w.seq;
+        step_body<ET, CPL, Q, BCPL, BQ>(D);
+    } else {
+        step_body<ET, CPL, Q, BCPL, BQ>(D0);
     }
 }
 

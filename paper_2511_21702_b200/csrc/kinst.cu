@@ -9,4 +9,5 @@ template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q>(Dev);
 template __global__ void k_step<KI_ET, KI_CPL, KI_Q, 0, 0>(Dev);
 #if KI_CPL > 0
 template __global__ void k_dense_gemv<KI_ET, KI_CPL, KI_Q>(Dev);
+template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q, true>(Dev);  // grouped batch lanes
 #endif
