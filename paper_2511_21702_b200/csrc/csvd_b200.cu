@@ -528,6 +528,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             ur[b] = ctx->lanes[b].D.Uraw;
             dt[b] = ctx->lanes[b].D.dots;
             ctx->lanes[b].D.pre_bounds = 1;
+            ctx->lanes[b].Dh.pre_bounds = 1;  // the host-I/O twin of the lane too
         }
         if ((rc = lalloc(ctx, &ctx->d_Uraw_l, B)) || (rc = lalloc(ctx, &ctx->d_dots_l, B))) return rc;
         CK(cudaMemcpy(ctx->d_Uraw_l, ur.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));

@@ -1375,29 +1375,24 @@ __device__ __forceinline__ bool head_eligible(const csvd_config &cfg) {
     return cfg.variant == CSVD_VARIANT_INCREMENTAL && cfg.first_wave_tokens <= 0;
 }
 
-// host-API steps: every CTA copies its slice of the final outputs to the
-// mapped host buffers; the last to arrive publishes the result struct and the
-// sequence number the host is spinning on.
+// host-API steps: CTA 0 copies the final outputs (complete in global memory:
+// every CTA reaches this point only after the last grid barrier) into the
+// mapped host buffers, then publishes the result struct and the sequence
+// number the host spins on.  One system fence per step: with every CTA fencing
+// its own slice, 144 concurrent system fences cost ~150 us in batched launches.
 static __device__ __noinline__ void publish_host(const Dev &D, long long n, const csvd_result *r_cta0) {
-    if (!D.res_host) return;
-    const long long per = (n + CTA_N - 1) / CTA_N;
-    const long long a = (long long)CTA_ID * per, b = min(n, a + per);
-    for (long long i = a + threadIdx.x; i < b; i += THREADS) {
+    if (!D.res_host || CTA_ID != 0) return;
+    for (long long i = threadIdx.x; i < n; i += THREADS) {
         D.ids_host[i] = __ldcg(D.S_ids + i);
         D.logits_host[i] = __ldcg(D.S_logits + i);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (r_cta0) *D.res_host = *r_cta0;
+        *D.res_host = *r_cta0;
+        const unsigned long long sq = *D.seq + 1;
+        *D.seq = sq;
         __threadfence_system();
-        const unsigned t = atomicAdd(D.done_ctas, 1u);
-        if (t == CTA_N - 1) {
-            *D.done_ctas = 0;
-            const unsigned long long sq = *D.seq + 1;
-            *D.seq = sq;
-            __threadfence_system();
-            *D.host_flag = sq;
-        }
+        *D.host_flag = sq;
     }
 }
 
