@@ -115,8 +115,9 @@ struct csvd_ctx {
     double **d_Uraw_l = nullptr, **d_dots_l = nullptr;  // [lanes] per-lane bound outputs
     kern_t kgroup = nullptr;                      // grouped lanes kernel (one launch per batch)
     LaneWS *d_lanes = nullptr, *d_lanes_host = nullptr;
-    void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *) = nullptr;
+    void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *, int) = nullptr;
     size_t kbb_smem = 0;
+    int kbb_gq = 0;
     cudaGraphExec_t g_batch = nullptr;
     int g_batch_B = 0, g_batch_host = 0;
     csvd_result *res_map_b = nullptr;  // [lanes] mapped
@@ -517,7 +518,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     ctx->kbb = nullptr;
     if (D0.bplan.regular && D0.bplan.cpl == 8 && D0.mode != CSVD_MODE_BIAS_AUGMENTED) {
         switch (D0.bplan.q) {
-            case 1: ctx->kbb = k_bounds_batch<1>; break;
+            case 1: ctx->kbb = k_bounds_batch<1>; break;  // fits any d with >= 1 query per pass
             case 2: ctx->kbb = k_bounds_batch<2>; break;
             case 4: ctx->kbb = k_bounds_batch<4>; break;
         }
@@ -533,7 +534,9 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         if ((rc = lalloc(ctx, &ctx->d_Uraw_l, B)) || (rc = lalloc(ctx, &ctx->d_dots_l, B))) return rc;
         CK(cudaMemcpy(ctx->d_Uraw_l, ur.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_dots_l, dt.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
-        ctx->kbb_smem = sizeof(double) * BQN * (size_t)((pw_hs_size(D0.bplan) + 1) & ~1);
+        const size_t hsb = sizeof(double) * (size_t)((pw_hs_size(D0.bplan) + 1) & ~1);
+        ctx->kbb_gq = (int)std::min<size_t>(BQN, (227 * 1024) / hsb);
+        ctx->kbb_smem = hsb * ctx->kbb_gq;
         CK(cudaFuncSetAttribute((const void *)ctx->kbb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ctx->kbb_smem));
     }
@@ -602,7 +605,7 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
         ctx->kbb<<<ctx->grid, THREADS, ctx->kbb_smem, s>>>(D0, ctx->d_H, B, ctx->d_Uraw_l, ctx->d_dots_l,
-                                                           ctx->d_res_all);
+                                                           ctx->d_res_all, ctx->kbb_gq);
         CK(cudaGetLastError());
     }
     if (ctx->kgroup) {  // every lane in one cooperative launch of B x G CTAs

@@ -1755,11 +1755,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
 // tree per query as bounds_phase); lanes then start from these bounds.
 // Regular plans only (the bound dimension is d: euclidean / spherical).
 // ---------------------------------------------------------------------------
-#define BQN 4
+#define BQN 7
 template <int BQ>
 __global__ void __launch_bounds__(THREADS, 1)
     k_bounds_batch(Dev D, const double *__restrict__ H, int B, double *const *Uraw_l, double *const *dots_l,
-                   csvd_result *res_all) {
+                   csvd_result *res_all, int gq /* queries per pass (<= BQN, by shared memory) */) {
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hs_stride = (pw_hs_size(D.bplan) + 1) & ~1;
@@ -1769,9 +1769,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
     if ((D.pf_mask & 1) && lane == 0)  // optional: this warp's centroid rows towards L2
         for (int c = gwarp; c < D.C; c += nwarps) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
-    for (int qb = 0; qb < B; qb += BQN) {
-        const int nq = min(BQN, B - qb);
-        tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / BQN));
+    for (int qb = 0; qb < B; qb += gq) {
+        const int nq = min(gq, B - qb);
+        tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / gq));
         for (int c = gwarp; c < D.C; c += nwarps) {
             double dots[BQN];
             warp_dot_regular_multi<BQ, BQN>(D.cent + (size_t)c * D.bd, smem, hs_stride, nq, D.bplan.leaf_len, lane,
