@@ -1755,7 +1755,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
 // tree per query as bounds_phase); lanes then start from these bounds.
 // Regular plans only (the bound dimension is d: euclidean / spherical).
 // ---------------------------------------------------------------------------
-#define BQN 7
+#define BQN 3
 template <int BQ>
 __global__ void __launch_bounds__(THREADS, 1)
     k_bounds_batch(Dev D, const double *__restrict__ H, int B, double *const *Uraw_l, double *const *dots_l,
@@ -1772,14 +1772,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int qb = 0; qb < B; qb += gq) {
         const int nq = min(gq, B - qb);
         tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / gq));
-        for (int c = gwarp; c < D.C; c += nwarps) {
-            double dots[BQN];
-            warp_dot_regular_multi<BQ, BQN>(D.cent + (size_t)c * D.bd, smem, hs_stride, nq, D.bplan.leaf_len, lane,
-                                            dots);
+        // two clusters per warp at a time: each staged query value read from
+        // shared memory feeds both rows
+        for (int c = gwarp; c < D.C; c += 2 * nwarps) {
+            const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
+            const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
+            double dots[2][BQN];
+            warp_dot_regular_multi<BQ, BQN, 2>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
             if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
 #pragma unroll
                 for (int j = 0; j < BQN; ++j)
-                    if (j < nq) dots_l[qb + j][c] = dots[j];
+                    if (j < nq) {
+                        dots_l[qb + j][c] = dots[0][j];
+                        if (c2 != c) dots_l[qb + j][c2] = dots[1][j];
+                    }
             }
         }
         __syncthreads();

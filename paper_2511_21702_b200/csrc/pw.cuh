@@ -238,30 +238,34 @@ __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
     return d_add(0.0, tot);
 }
 
-// Same tree as warp_dot_regular<double, 8, Q>, for NQ queries at once: every
-// row element is loaded once and multiplied into NQ accumulator sets, so a
-// batch of queries shares each centroid read (batched bounds).
-template <int Q, int NQ>
-__device__ __forceinline__ void warp_dot_regular_multi(const double *__restrict__ row,
+// Same tree as warp_dot_regular<double, 8, Q>, for NR rows x NQ queries at
+// once: every row element is loaded once and every staged query value is read
+// once per NR rows (batched bounds: centroid reads shared by the queries,
+// shared-memory reads of h shared by the rows).  out[r][j] = row r . query j.
+template <int Q, int NQ, int NR>
+__device__ __forceinline__ void warp_dot_regular_multi(const double *const (&rows)[NR],
                                                        const double *__restrict__ hs0, int hs_stride, int nq,
-                                                       int leaf_len, int lane, double (&out)[NQ]) {
-    constexpr int NB = 4;
+                                                       int leaf_len, int lane, double (&out)[NR][NQ]) {
+    constexpr int NB = 2;
     const int S = leaf_len >> 3;
-    double slice[NQ][Q];
+    double slice[NR][NQ][Q];
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
-        const double *lp = row + (size_t)(u * 32 + lane) * leaf_len;
         const double *hp = hs0 + (size_t)(u * 32 + lane) * (leaf_len + 2);
-        double r[NQ][8];
+        double r[NR][NQ][8];
 #pragma unroll
-        for (int j = 0; j < NQ; ++j)
+        for (int w = 0; w < NR; ++w)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) r[j][c] = 0.0;
+            for (int j = 0; j < NQ; ++j)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) r[w][j][c] = 0.0;
         for (int i0 = 0; i0 < S; i0 += NB) {
-            Raw<double, 8> raw[NB];
+            Raw<double, 8> raw[NR][NB];
 #pragma unroll
-            for (int s = 0; s < NB; ++s)
-                if (i0 + s < S) raw[s].load(lp + (i0 + s) * 8);
+            for (int w = 0; w < NR; ++w)
+#pragma unroll
+                for (int s = 0; s < NB; ++s)
+                    if (i0 + s < S) raw[w][s].load(rows[w] + (size_t)(u * 32 + lane) * leaf_len + (i0 + s) * 8);
 #pragma unroll
             for (int s = 0; s < NB; ++s) {
                 if (i0 + s < S) {
@@ -278,35 +282,41 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *__restrict_
                                 hv[2 * c2 + 1] = t.y;
                             }
 #pragma unroll
-                            for (int c = 0; c < 8; ++c) {
-                                const double pr = d_mul(raw[s].get(c), hv[c]);
-                                r[j][c] = (i == 0) ? pr : d_add(r[j][c], pr);
-                            }
+                            for (int w = 0; w < NR; ++w)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) {
+                                    const double pr = d_mul(raw[w][s].get(c), hv[c]);
+                                    r[w][j][c] = (i == 0) ? pr : d_add(r[w][j][c], pr);
+                                }
                         }
                     }
                 }
             }
         }
 #pragma unroll
+        for (int w = 0; w < NR; ++w)
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+                double v = d_add(d_add(d_add(r[w][j][0], r[w][j][1]), d_add(r[w][j][2], r[w][j][3])),
+                                 d_add(d_add(r[w][j][4], r[w][j][5]), d_add(r[w][j][6], r[w][j][7])));
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
+                slice[w][j][u] = v;
+            }
+    }
+#pragma unroll
+    for (int w = 0; w < NR; ++w)
+#pragma unroll
         for (int j = 0; j < NQ; ++j) {
-            double v = d_add(d_add(d_add(r[j][0], r[j][1]), d_add(r[j][2], r[j][3])),
-                             d_add(d_add(r[j][4], r[j][5]), d_add(r[j][6], r[j][7])));
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
-            slice[j][u] = v;
+            double tot;
+            if constexpr (Q == 1)
+                tot = slice[w][j][0];
+            else if constexpr (Q == 2)
+                tot = d_add(slice[w][j][0], slice[w][j][1]);
+            else
+                tot = d_add(d_add(slice[w][j][0], slice[w][j][1]), d_add(slice[w][j][2], slice[w][j][3]));
+            out[w][j] = d_add(0.0, tot);
         }
-    }
-#pragma unroll
-    for (int j = 0; j < NQ; ++j) {
-        double tot;
-        if constexpr (Q == 1)
-            tot = slice[j][0];
-        else if constexpr (Q == 2)
-            tot = d_add(slice[j][0], slice[j][1]);
-        else
-            tot = d_add(d_add(slice[j][0], slice[j][1]), d_add(slice[j][2], slice[j][3]));
-        out[j] = d_add(0.0, tot);
-    }
 }
 
 // ||h||^2 in the CPL = 8 pairwise order with both operands from the staged
