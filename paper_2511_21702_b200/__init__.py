@@ -35,6 +35,7 @@ from .engine import (
     decode_step_batchselect,
     dense_logits,
     prepare,
+    refined_bias_bound,
 )
 from .shard import CommLedger, LatencyModel, ShardPlan, make_plan, sharded_decode_step
 from . import formats
@@ -47,7 +48,7 @@ __all__ = [
     "BoundVector", "CertStatus", "ClusterIndex", "ClusterMeta", "ConfigError", "DecodeConfig",
     "DecodeOutcome", "DenseResult", "EmbeddingTable", "FingerprintMismatchError", "FullVocab",
     "PartialExpand", "RelaxEps", "StepMetrics", "DeviceIndex", "clear_cache", "cluster_bounds",
-    "decode_step", "decode_step_batch", "decode_step_batchselect", "dense_logits", "prepare", "CommLedger",
+    "decode_step", "decode_step_batch", "decode_step_batchselect", "dense_logits", "prepare", "refined_bias_bound", "CommLedger",
     "LatencyModel", "ShardPlan", "make_plan", "sharded_decode_step", "AdaptiveBudget", "BudgetedDecoder",
     "FlopReport", "adapt_budget", "flop_accounting", "flop_report", "warmup_k_max",
 ]

@@ -425,3 +425,29 @@ def dense_logits(table, h) -> DenseResult:
     probs = np.exp(logits - lse)
     order = np.lexsort((np.arange(logits.size), -logits))
     return DenseResult(logits=logits, probs=probs, order=order)
+
+
+def refined_bias_bound(index, c: int, h, exclude: set, bias=None) -> float:
+    """B200 `csvd.refined_bias_bound` (bounds.py:187-220): cluster c's bound
+    with the max-bias term restricted to unopened members.
+
+    The geometric part is the device bound minus the cluster's max bias, the
+    same subtraction the reference performs on its raw bound; the bias term
+    comes from the top-m table (the first entry not excluded), else the exact
+    remaining maximum when `bias` is given, else the m-th tabled value (still
+    an upper bound on every untabled member).  -inf when every member is
+    excluded."""
+    if index.mode == "bias_augmented":
+        raise ValueError("bias refinement does not apply to bias_augmented indexes")
+    members = index.members(c)
+    remaining = [int(t) for t in members if int(t) not in exclude]
+    if not remaining:
+        return NEG_INF
+    meta = index.clusters[c]
+    geom = float(cluster_bounds(index, h).values[c]) - meta.max_bias
+    for value, token in meta.bias_topm:
+        if token not in exclude:
+            return geom + value
+    if bias is not None:
+        return geom + float(max(bias[t] for t in remaining))
+    return geom + meta.bias_topm[-1][0]

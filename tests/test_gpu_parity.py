@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import csvd_oracle as O
-from conftest import TRANS_RTOL, GoldenCase, assert_outcome, golden_names, has_gpu
+from conftest import TRANS_RTOL, GoldenCase, assert_outcome, close, golden_names, has_gpu
 import paper_2511_21702_b200 as P
 from paper_2511_21702_b200 import workload as wl
 
@@ -174,3 +174,30 @@ def test_files_to_device_step(tmp_path):
     for i, h in enumerate(q):
         assert_outcome(P.decode_step(T2, ix2, h, cfg), _fields(O.decode_step(T, ix, h, cfg)), rtol=TRANS_RTOL,
                        where=f"files[{i}]")
+
+
+@pytest.mark.parametrize("mode", ["euclidean", "spherical"])
+def test_refined_bias_bound_matches_oracle_and_reference_rules(mode):
+    """refined_bias_bound (bounds.py:187-220): no exclusion gives the plain bound,
+    excluding the top tabled token gives geom + the second tabled bias, and
+    excluding every tabled token falls back to the exact remaining max (with
+    `bias`) or the m-th tabled value (without)."""
+    T = wl.synth_vocab(3000, 64, 12, 0.4, 3)
+    ix = wl.fast_index(T, 12, 2, mode=mode)
+    h = wl.generate_queries(1, 64, "random", 4)[0]
+    U = O.cluster_bounds(ix, h).values
+    for c in range(ix.n_clusters):
+        meta = ix.clusters[c]
+        geom = U[c] - meta.max_bias
+        tol = 0.0 if mode == "euclidean" else 1e-12
+        assert close(P.refined_bias_bound(ix, c, h, set()), U[c], tol)
+        if len(meta.bias_topm) >= 2:
+            got = P.refined_bias_bound(ix, c, h, {meta.bias_topm[0][1]})
+            assert close(got, geom + meta.bias_topm[1][0], tol)
+        tabled = {t for _, t in meta.bias_topm}
+        members = [int(t) for t in ix.members(c)]
+        if len(members) > len(tabled):
+            rest = max(T.bias[t] for t in members if t not in tabled)
+            assert close(P.refined_bias_bound(ix, c, h, tabled, bias=T.bias), geom + rest, tol)
+            assert close(P.refined_bias_bound(ix, c, h, tabled), geom + meta.bias_topm[-1][0], tol)
+        assert P.refined_bias_bound(ix, c, h, set(members)) == float("-inf")
