@@ -1559,7 +1559,16 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
     __shared__ ScanShared ss;
     const bool lead = CTA_ID == 0 && threadIdx.x == 0;
     if (lead) DBG_TS(D, 0);
-    if (D.launch_mode != LAUNCH_BOUNDS) pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
+    if (D.launch_mode != LAUNCH_BOUNDS) {
+        if constexpr (CPL == 8) {  // one TMA bulk copy per pairwise leaf, completion on an mbarrier
+            __shared__ unsigned long long s_hbar;
+            if (threadIdx.x == 0) mbar_init(&s_hbar, 1);
+            __syncthreads();
+            tma_stage_leaves(D.wplan, D.h, D.d, 1, hs_w, 0, &s_hbar, 0);
+        } else {
+            pw_stage<CPL>(D.wplan, D.h, D.d, hs_w, D.wsrc);
+        }
+    }
     if (!D.pre_bounds && (D.launch_mode == LAUNCH_BOUNDS || D.hs_off_b))
         pw_stage<BCPL>(D.bplan, D.h, D.d, hs_b, D.bsrc);
     if (D.launch_mode != LAUNCH_DENSE && !D.pre_bounds && (D.pf_mask & 1) && lane == 0) {

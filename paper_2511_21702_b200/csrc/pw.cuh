@@ -145,7 +145,7 @@ template <> struct Raw<double, 1> {
 
 // loads in flight per lane per batch (register budget ~64 regs of raw data)
 template <typename ET, int CPL> struct NBatch { static constexpr int value = 8; };
-template <int CPL> struct NBatch<double, CPL> { static constexpr int value = (CPL >= 8 ? 4 : 8); };
+template <int CPL> struct NBatch<double, CPL> { static constexpr int value = 8; };
 template <int CPL> struct NBatch<uint16_t, CPL> { static constexpr int value = 16; };
 
 // ---------------------------------------------------------------------------
