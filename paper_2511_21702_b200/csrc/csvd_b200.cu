@@ -85,8 +85,6 @@ struct csvd_ctx {
     csvd_result *res_map = nullptr;
     long long *ids_map = nullptr;
     double *logits_map = nullptr;
-    unsigned long long *flag_map = nullptr;
-    unsigned long long seq_host = 0;
     Dev Dhost{};
     int direct = 0;
     void *flush_buf = nullptr;
@@ -123,8 +121,6 @@ struct csvd_ctx {
     csvd_result *res_map_b = nullptr;  // [lanes] mapped
     long long *ids_map_b = nullptr;    // [lanes, V] mapped
     double *logits_map_b = nullptr;    // [lanes, V] mapped
-    unsigned long long *flags_b = nullptr;
-    unsigned long long batch_seq = 0;
 };
 
 static int fail(csvd_ctx *c, int code, const std::string &msg) {
@@ -388,8 +384,6 @@ static int build_graphs(csvd_ctx *ctx) {
         H.ids_host = (long long *)p;
         CK(cudaHostGetDevicePointer(&p, ctx->logits_map, 0));
         H.logits_host = (double *)p;
-        CK(cudaHostGetDevicePointer(&p, ctx->flag_map, 0));
-        H.host_flag = (volatile unsigned long long *)p;
     }
     for (cudaGraphExec_t *g : {&ctx->g_step, &ctx->g_host, &ctx->g_bounds, &ctx->g_dense}) {
         if (*g) cudaGraphExecDestroy(*g);
@@ -422,13 +416,11 @@ static void free_lanes(csvd_ctx *ctx) {
     if (ctx->res_pin_b) cudaFreeHost(ctx->res_pin_b);
     if (ctx->ids_pin_b) cudaFreeHost(ctx->ids_pin_b);
     if (ctx->logits_pin_b) cudaFreeHost(ctx->logits_pin_b);
-    for (void *p : {(void *)ctx->res_map_b, (void *)ctx->ids_map_b, (void *)ctx->logits_map_b, (void *)ctx->flags_b})
+    for (void *p : {(void *)ctx->res_map_b, (void *)ctx->ids_map_b, (void *)ctx->logits_map_b})
         if (p) cudaFreeHost(p);
     ctx->res_map_b = nullptr;
     ctx->ids_map_b = nullptr;
     ctx->logits_map_b = nullptr;
-    ctx->flags_b = nullptr;
-    ctx->batch_seq = 0;
     ctx->H_pin = nullptr;
     ctx->res_pin_b = nullptr;
     ctx->ids_pin_b = nullptr;
@@ -467,8 +459,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     CK(cudaHostAlloc(&ctx->res_map_b, sizeof(csvd_result) * B, cudaHostAllocMapped));
     CK(cudaHostAlloc(&ctx->ids_map_b, sizeof(long long) * B * (size_t)V, cudaHostAllocMapped));
     CK(cudaHostAlloc(&ctx->logits_map_b, sizeof(double) * B * (size_t)V, cudaHostAllocMapped));
-    CK(cudaHostAlloc(&ctx->flags_b, sizeof(unsigned long long) * B, cudaHostAllocMapped));
-    memset(ctx->flags_b, 0, sizeof(unsigned long long) * B);
     ctx->lanes.resize(B);
     for (int b = 0; b < B; ++b) {
         Lane &l = ctx->lanes[b];
@@ -492,10 +482,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         L.res_host = nullptr;
         L.ids_host = nullptr;
         L.logits_host = nullptr;
-        L.host_flag = nullptr;
-        if ((rc = lalloc(ctx, &L.done_ctas, 1)) || (rc = lalloc(ctx, &L.seq, 1))) return rc;
-        CK(cudaMemset(L.done_ctas, 0, sizeof(unsigned)));
-        CK(cudaMemset(L.seq, 0, sizeof(unsigned long long)));
         l.D = L;
         {
             Dev Hl = L;
@@ -506,8 +492,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             Hl.ids_host = (long long *)p;
             CK(cudaHostGetDevicePointer(&p, ctx->logits_map_b + (size_t)b * V, 0));
             Hl.logits_host = (double *)p;
-            CK(cudaHostGetDevicePointer(&p, ctx->flags_b + b, 0));
-            Hl.host_flag = (volatile unsigned long long *)p;
             l.Dh = Hl;
         }
         CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
@@ -564,9 +548,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             w.res_host = L.res_host;
             w.ids_host = L.ids_host;
             w.logits_host = L.logits_host;
-            w.host_flag = L.host_flag;
-            w.done_ctas = L.done_ctas;
-            w.seq = L.seq;
             return w;
         };
         std::vector<LaneWS> td(B), th(B);
@@ -600,7 +581,7 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     cudaGraph_t g;
     const Dev &D0 = ctx->D;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    if (host_io && !getenv("CSVD_BATCH_H_OUTSIDE"))
+    if (host_io)
         CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
@@ -685,40 +666,28 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto t0 = now();
     memcpy(ctx->H_pin, H, sizeof(double) * B * ctx->D.d);
-    const unsigned long long want = ++ctx->batch_seq;
-    static const bool h_outside = getenv("CSVD_BATCH_H_OUTSIDE") != nullptr;
-    if (h_outside) CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * ctx->D.d, cudaMemcpyHostToDevice, s));
+    for (int b = 0; b < B; ++b) ctx->res_map_b[b].kind = CSVD_KIND_NONE - 1;  // sentinels, overwritten by the lanes
     auto t1 = now();
     CK(cudaGraphLaunch(ctx->g_batch, s));
     auto t2 = now();
-    // every lane publishes its result into mapped memory and bumps its flag
-    static const bool sync_wait = getenv("CSVD_BATCH_SYNC") != nullptr;
-    if (sync_wait) CK(cudaStreamSynchronize(s));
-    volatile unsigned long long *flags = ctx->flags_b;
-    int ready = 0;
-    for (unsigned long long spins = 0; ready < B; ++spins) {
-        ready = 0;
-        for (int b = 0; b < B; ++b) ready += flags[b] == want;
-        if (ready < B && (spins & 255) == 255 && cudaStreamQuery(s) != cudaErrorNotReady) {
-            ready = 0;
-            for (int b = 0; b < B; ++b) ready += flags[b] == want;
-            break;
-        }
+    // every lane publishes its result into mapped memory; busy-poll the stream
+    cudaError_t q;
+    while ((q = cudaStreamQuery(s)) == cudaErrorNotReady) {
     }
+    if (q != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("batch: ") + cudaGetErrorString(q));
+    int ready = 0;
+    for (int b = 0; b < B; ++b) ready += ctx->res_map_b[b].kind != CSVD_KIND_NONE - 1;
     if (ready < B) {  // a lane ended without publishing: device error
         CK(cudaStreamSynchronize(s));
         std::vector<csvd_result> rr(B);
         CK(cudaMemcpy(rr.data(), ctx->d_res_all, sizeof(csvd_result) * B, cudaMemcpyDeviceToHost));
         bool value_err = false;
         for (auto &r : rr) value_err = value_err || r.error == CSVD_EVALUE;
-        ctx->batch_seq = 0;
-        for (int b = 0; b < B; ++b) ctx->flags_b[b] = 0;
+
         CK(cudaMemset(ctx->d_res_all, 0, sizeof(csvd_result) * B));
         for (Lane &l : ctx->lanes) {
             CK(cudaMemset(l.D.bar, 0, 16));
             CK(cudaMemset(l.D.cnt, 0, sizeof(int) * ctx->D.C));
-            CK(cudaMemset(l.D.seq, 0, sizeof(unsigned long long)));
-            CK(cudaMemset(l.D.done_ctas, 0, sizeof(unsigned)));
         }
         if (value_err) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
         return fail(ctx, CSVD_ESTATE, "device state error in a batch lane (grid barrier timeout)");
@@ -977,16 +946,9 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     CK(cudaHostAlloc(&ctx->res_map, sizeof(csvd_result), cudaHostAllocMapped));
     CK(cudaHostAlloc(&ctx->ids_map, sizeof(long long) * V, cudaHostAllocMapped));
     CK(cudaHostAlloc(&ctx->logits_map, sizeof(double) * V, cudaHostAllocMapped));
-    CK(cudaHostAlloc(&ctx->flag_map, sizeof(unsigned long long), cudaHostAllocMapped));
-    *ctx->flag_map = 0;
     D.res_host = nullptr;
     D.ids_host = nullptr;
     D.logits_host = nullptr;
-    D.host_flag = nullptr;
-    if ((rc = dalloc(ctx, &D.done_ctas, 1))) return rc;
-    if ((rc = dalloc(ctx, &D.seq, 1))) return rc;
-    CK(cudaMemset(D.done_ctas, 0, sizeof(unsigned)));
-    CK(cudaMemset(D.seq, 0, sizeof(unsigned long long)));
     D.K = 32;
     if ((rc = configure(ctx))) return rc;
     if ((rc = alloc_k(ctx, 32))) return rc;
@@ -1021,7 +983,7 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     if (ctx->res_pin) cudaFreeHost(ctx->res_pin);
     if (ctx->ids_pin) cudaFreeHost(ctx->ids_pin);
     if (ctx->logits_pin) cudaFreeHost(ctx->logits_pin);
-    for (void *p : {(void *)ctx->res_map, (void *)ctx->ids_map, (void *)ctx->logits_map, (void *)ctx->flag_map})
+    for (void *p : {(void *)ctx->res_map, (void *)ctx->ids_map, (void *)ctx->logits_map})
         if (p) cudaFreeHost(p);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1098,26 +1060,19 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         CK(cudaMemcpyAsync(ctx->logits_pin, ctx->D.S_logits, sizeof(double) * first, cudaMemcpyDeviceToHost, s));
     } else {
         // zero-copy: the kernel writes ids / logits / result into mapped host
-        // memory and raises the flag; spin on it instead of a stream sync
-        const unsigned long long want = ++ctx->seq_host;
+        // memory; busy-poll the stream (no blocking-sync wake-up) and read them
+        // once the kernel has completed
         static const bool prof = getenv("CSVD_PROFILE_HOST") != nullptr;
         auto t1 = std::chrono::steady_clock::now();
+        ctx->res_map->kind = CSVD_KIND_NONE - 1;  // sentinel: overwritten by the kernel
         CK(cudaGraphLaunch(ctx->g_host, s));
         auto t2 = std::chrono::steady_clock::now();
-        volatile unsigned long long *flag = ctx->flag_map;
-        bool got = false;
-        for (unsigned long long spins = 0;; ++spins) {
-            if (*flag == want) {
-                got = true;
-                break;
-            }
-            if ((spins & 255) == 255 && cudaStreamQuery(s) != cudaErrorNotReady) {
-                got = *flag == want;
-                break;
-            }
+        cudaError_t q;
+        while ((q = cudaStreamQuery(s)) == cudaErrorNotReady) {
         }
+        if (q != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("step: ") + cudaGetErrorString(q));
+        const bool got = ctx->res_map->kind != CSVD_KIND_NONE - 1;
         if (got) {
-            std::atomic_thread_fence(std::memory_order_acquire);
             if (prof) {
                 auto t3 = std::chrono::steady_clock::now();
                 auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -1132,8 +1087,6 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
             return 0;
         }
         // the step ended without publishing (device error): read its state
-        --ctx->seq_host;
-        CK(cudaStreamSynchronize(s));
         CK(cudaMemcpy(ctx->res_pin, ctx->D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost));
         *res = *ctx->res_pin;
         if ((rc = result_error(ctx, *res))) return rc;
