@@ -77,6 +77,8 @@ struct csvd_ctx {
     double *d_h = nullptr;
     double *h_pin = nullptr;
     csvd_config *cfg_pin = nullptr;
+    csvd_config cfg_dev{};   // the config currently resident in d_cfg
+    bool cfg_valid = false;
     csvd_result *res_pin = nullptr;
     long long *ids_pin = nullptr;
     double *logits_pin = nullptr;
@@ -360,7 +362,10 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    // step graphs carry no config upload: the config is uploaded only when it
+    // changes (sync_cfg), so an unchanged config costs no copy node per step
+    if (mode != LAUNCH_STEP)
+        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     // host I/O: the kernel itself writes the result into mapped host memory
     int rc = launch(ctx, mode, s, host_io);
     if (rc) {
@@ -632,6 +637,7 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
 }
 
 static int batch_prepare(csvd_ctx *ctx, int B, const csvd_config *cfg, bool host_io) {
+    if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (B < 1 || B > 1024) return fail(ctx, CSVD_ECONFIG, "batch size must be in [1, 1024]");
     int rc = check_cfg(ctx, cfg);
     if (rc) return rc;
@@ -931,8 +937,8 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     D.pre_bounds = 0;
     D.lanes = nullptr;
     if (getenv("CSVD_DEBUG_TS") && atoi(getenv("CSVD_DEBUG_TS")) > 0) {
-        if ((rc = dalloc(ctx, &D.dbg, 128))) return rc;
-        CK(cudaMemset(D.dbg, 0, 128 * 8));
+        if ((rc = dalloc(ctx, &D.dbg, 128 + 512))) return rc;  // + per-CTA start / end times
+        CK(cudaMemset(D.dbg, 0, (128 + 512) * 8));
     }
     CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device));
     // --- pinned staging
@@ -1015,6 +1021,20 @@ static int result_error(csvd_ctx *ctx, const csvd_result &r) {
     return fail(ctx, r.error, "device state error (grid barrier timeout)");
 }
 
+// make d_cfg hold *cfg (stream-ordered, synchronous on change: configs rarely
+// change between steps, and a pinned staging buffer must not be rewritten
+// while an earlier upload is still queued)
+static int sync_cfg(csvd_ctx *ctx, const csvd_config *cfg, cudaStream_t s) {
+    if (ctx->cfg_valid && memcmp(&ctx->cfg_dev, cfg, sizeof(csvd_config)) == 0) return 0;
+    CK(cudaStreamSynchronize(s));
+    *ctx->cfg_pin = *cfg;
+    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->cfg_dev = *cfg;
+    ctx->cfg_valid = true;
+    return 0;
+}
+
 extern "C" int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_config *cfg, void *stream) {
     if (!ctx || !cfg) return CSVD_ESTATE;
     cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
@@ -1023,11 +1043,8 @@ extern "C" int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_c
     if (rc) return rc;
     if (h_dev && h_dev != ctx->d_h)
         CK(cudaMemcpyAsync(ctx->d_h, h_dev, sizeof(double) * ctx->D.d, cudaMemcpyDeviceToDevice, s));
-    *ctx->cfg_pin = *cfg;
-    if (ctx->direct) {
-        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
-        return launch(ctx, LAUNCH_STEP, s);
-    }
+    if ((rc = sync_cfg(ctx, cfg, s))) return rc;
+    if (ctx->direct) return launch(ctx, LAUNCH_STEP, s);
     CK(cudaGraphLaunch(ctx->g_step, s));
     return 0;
 }
@@ -1049,11 +1066,10 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
     if (rc) return rc;
     const int d = ctx->D.d;
     const int64_t first = ctx->first_chunk;
+    if ((rc = sync_cfg(ctx, cfg, s))) return rc;
     memcpy(ctx->h_pin, h, sizeof(double) * d);
-    *ctx->cfg_pin = *cfg;
     if (ctx->direct) {
         CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * d, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
         if ((rc = launch(ctx, LAUNCH_STEP, s))) return rc;
         CK(cudaMemcpyAsync(ctx->res_pin, ctx->D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->ids_pin, ctx->D.S_ids, sizeof(long long) * first, cudaMemcpyDeviceToHost, s));
@@ -1123,6 +1139,7 @@ static void fixed_cfg(csvd_config *cfg, long long V, int slack_f32) {
 extern "C" int csvd_bounds_host(csvd_ctx *ctx, const double *h, int32_t slack_f32, double *values, double *qn,
                                 double *slack) {
     if (!ctx || !h) return CSVD_ESTATE;
+    if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     fixed_cfg(ctx->cfg_pin, ctx->D.V, slack_f32);
@@ -1144,6 +1161,7 @@ extern "C" int csvd_bounds_host(csvd_ctx *ctx, const double *h, int32_t slack_f3
 }
 
 static int dense_async(csvd_ctx *ctx, cudaStream_t s) {
+    if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (!ctx->D.W) return fail(ctx, CSVD_ECONFIG, "bounds-only context (no table)");
     fixed_cfg(ctx->cfg_pin, ctx->D.V, 0);
     if (ctx->direct) {
@@ -1184,6 +1202,7 @@ extern "C" int csvd_dense_device(csvd_ctx *ctx, const double *h_dev, void *strea
 // ---------------------------------------------------------------------------
 extern "C" int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config *cfg, double *summary,
                                int64_t *positions, int64_t *ids, double *logits, int64_t cap, int64_t *n_out) {
+    if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (!ctx || !h || !cfg || !summary || !n_out) return CSVD_ESTATE;
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1237,6 +1256,7 @@ extern "C" int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config
 
 extern "C" int csvd_shard_dense(csvd_ctx *ctx, const double *h, int32_t k, double *summary, int64_t *ids,
                                 double *logits, int64_t cap, int64_t *n_out) {
+    if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (!ctx || !h || !summary || !n_out) return CSVD_ESTATE;
     if (!ctx->shard) return fail(ctx, CSVD_ECONFIG, "not a shard context");
     CK(cudaSetDevice(ctx->device));
@@ -1308,7 +1328,7 @@ extern "C" int csvd_l2_flush(csvd_ctx *ctx, void *stream) {
 extern "C" int csvd_debug_timestamps(csvd_ctx *ctx, unsigned long long *out64) {
     if (!ctx || !ctx->D.dbg) return CSVD_ESTATE;
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out64, ctx->D.dbg, 128 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out64, ctx->D.dbg, (128 + 512) * 8, cudaMemcpyDeviceToHost));
     return 0;
 }
 

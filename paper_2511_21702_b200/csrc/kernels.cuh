@@ -1740,7 +1740,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
         D.logits_host = w.logits_host;
         step_body<ET, CPL, Q, BCPL, BQ>(D);
     } else {
+        if (D0.dbg && threadIdx.x == 0) D0.dbg[128 + blockIdx.x] = gtimer();
         step_body<ET, CPL, Q, BCPL, BQ>(D0);
+        __syncthreads();
+        if (D0.dbg && threadIdx.x == 0) D0.dbg[128 + 256 + blockIdx.x] = gtimer();
     }
 }
 

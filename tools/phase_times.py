@@ -28,7 +28,7 @@ for w in range(4):
     names.update({8 + 4 * w: f"wave{w} rows start", 9 + 4 * w: f"wave{w} barrier passed",
                   10 + 4 * w: f"wave{w} summaries loaded", 11 + 4 * w: f"wave{w} scan+plan done"})
 for i, h in enumerate(q):
-    buf = np.zeros(128, dtype=np.uint64)
+    buf = np.zeros(128 + 512, dtype=np.uint64)
     import ctypes as C_
     if not os.environ.get("NOFLUSH"):
         lib.csvd_l2_flush(ctx._ctx, None)
@@ -37,6 +37,14 @@ for i, h in enumerate(q):
     if i < 2:
         continue
     t0 = int(buf[0])
+    nb = ctx.info()["grid_ctas"]
+    st_ = buf[128:128 + nb].astype(np.int64)
+    en_ = buf[384:384 + nb].astype(np.int64)
+    if st_.all() and en_.all():
+        t0_ = int(buf[0])
+        print(f"CTA starts: first {(st_.min() - t0_) / 1e3:.2f} last {(st_.max() - t0_) / 1e3:.2f} us; "
+              f"CTA ends: first {(en_.min() - t0_) / 1e3:.2f} median {(np.median(en_) - t0_) / 1e3:.2f} "
+              f"last {(en_.max() - t0_) / 1e3:.2f} us (slowest CTA {int(en_.argmax())})")
     print(f"head n = {int(buf[63])}")
     buf[63] = 0
     print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} fb={out.fallback_used}")
