@@ -104,7 +104,6 @@ struct csvd_ctx {
     std::vector<Lane> lanes;
     std::vector<void *> lane_allocs;
     int lane_grid = 0, lane_K = 0;
-    int lane_plain = 0;  // CSVD_LANE_PLAIN=1: lanes as plain launches (experiment)
     double *d_H = nullptr;                 // [lanes, d]
     csvd_result *d_res_all = nullptr;      // [lanes]
     double *H_pin = nullptr;
@@ -574,7 +573,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     }
     ctx->lane_grid = G;
     ctx->lane_K = K;
-    ctx->lane_plain = getenv("CSVD_LANE_PLAIN") && atoi(getenv("CSVD_LANE_PLAIN")) > 0 && B * G <= ctx->nsm;
     return 0;
 }
 
@@ -614,17 +612,9 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
         CK(cudaStreamWaitEvent(l.stream, ctx->fork, 0));
         Dev Dl = host_io ? l.Dh : l.D;  // host I/O: each lane publishes into mapped memory
         Dl.launch_mode = LAUNCH_STEP;
-        if (ctx->lane_plain) {
-            // plain launch: B lanes x grid CTAs <= one CTA per SM, so every lane's
-            // CTAs are co-resident anyway (the grid barrier times out, not hangs,
-            // if they ever were not)
-            ctx->kern<<<ctx->lane_grid, THREADS, ctx->smem, l.stream>>>(Dl);
-            CK(cudaGetLastError());
-        } else {
-            void *args[] = {&Dl};
-            CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->lane_grid), dim3(THREADS), args,
-                                           ctx->smem, l.stream));
-        }
+        void *args[] = {&Dl};
+        CK(cudaLaunchCooperativeKernel((const void *)ctx->kern, dim3(ctx->lane_grid), dim3(THREADS), args, ctx->smem,
+                                       l.stream));
         CK(cudaEventRecord(l.done, l.stream));
         CK(cudaStreamWaitEvent(s, l.done, 0));
     }
