@@ -502,7 +502,7 @@ __device__ __forceinline__ bool okey_before(unsigned long long ka, int ia, unsig
 // p = n needs).  Returns n, or 0 when the head does not apply (more than 64
 // clusters, or a residual sum too small for the direct form): then the full
 // sort runs instead.
-static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
+static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, double &est_out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = D.C;
     const double *__restrict__ Us = o.Us;
@@ -551,6 +551,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o) {
     __syncthreads();
     const int c0 = s_i[0];
     const double est = s_est;
+    if (threadIdx.x == 0) est_out = est;  // init_state's wave estimate, already known here
     // --- membership, x = log|c| + U (certify.py:119), best non-head cluster
     double xm = -INFINITY;
     bk = ~0ull;
@@ -1325,7 +1326,8 @@ static __device__ __forceinline__ double block_kth_largest(const double *vals, i
 // head_n > 0: only positions [0, head_n] of the ordering exist yet (order_head);
 // the first wave is the head, and the budget cap is computed once the full
 // order exists (the kernel builds it before planning past the head).
-static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, ScanShared &ss, int head_n) {
+static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, ScanShared &ss, int head_n,
+                                                  double head_est) {
     const csvd_config &cfg = *D.cfg;
     ScanState st;
     memset(&st, 0, sizeof(st));
@@ -1348,8 +1350,9 @@ static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, Sc
     const long long wt = cfg.first_wave_tokens > 0 ? cfg.first_wave_tokens : 1;
     st.wave_tokens = (int)min(wt, (long long)D.V);
     const int c0 = o.order[0];
-    st.est = (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? __ldcg(D.dots + c0)
-                                                  : __dadd_rn(__ldcg(D.dots + c0), D.meanb[c0]);
+    st.est = head_n > 0 ? head_est  // the same value order_head computed for c0
+                        : (D.mode == CSVD_MODE_BIAS_AUGMENTED) ? __ldcg(D.dots + c0)
+                                                               : __dadd_rn(__ldcg(D.dots + c0), D.meanb[c0]);
     st.p_lo = 0;
     st.p_hi = head_n > 0 ? head_n : csvd_plan_wave(st, in, search);
     st.mode = MODE_SPARSE;
@@ -1605,12 +1608,13 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
             if (lead) D.res->error = ok ? 0 : CSVD_EVALUE;
             return;
         }
-        const int hn = head_eligible(*D.cfg) ? order_head(D, o) : 0;
+        __shared__ double s_head_est;
+        const int hn = head_eligible(*D.cfg) ? order_head(D, o, s_head_est) : 0;
         if (lead && D.dbg) D.dbg[63] = (unsigned long long)hn;
         if (lead) DBG_TS(D, 5);
         if (hn == 0) order_full(D, o);
         if (lead) DBG_TS(D, 4);
-        if (threadIdx.x == 0) init_state(D, o, ss, hn);
+        if (threadIdx.x == 0) init_state(D, o, ss, hn, s_head_est);
         __syncthreads();
         if (lead) DBG_TS(D, 6);
         if (D.launch_mode == LAUNCH_SHARD) {
