@@ -39,3 +39,22 @@ def test_batch_equals_independent_steps(B, dtype):
             one = P.decode_step(T, ix, H[b], cfg)
             assert np.array_equal(one.token_ids, outs[b].token_ids)
             assert np.array_equal(one.logits, outs[b].logits)
+
+
+@pytest.mark.parametrize("mode", ["spherical", "bias_augmented"])
+def test_batch_other_bound_modes(mode):
+    """Spherical (batched dots + cone bound in the lanes) and bias-augmented
+    (d+1 bound rows: no batched bounds, forked lanes with their own bounds)."""
+    import paper_2511_21702_b200 as P
+    from paper_2511_21702_b200 import workload as wl
+    d = 512
+    T = wl.synth_vocab(12000, d, 60, 0.3, 1)
+    ix = wl.fast_index(T, 60, 2, mode=mode)
+    H = np.vstack([wl.generate_queries(5, d, "contextual", 7, centroids=ix.centroids[:, :d]),
+                   wl.generate_queries(2, d, "random", 8)])
+    for cfg in (P.DecodeConfig(k=10), P.DecodeConfig(k=5, epsilon=1e-2, targets=("softmax_eps",))):
+        outs = P.decode_step_batch(T, ix, H, cfg)
+        for b in range(len(H)):
+            exp = O.decode_step(T, ix, H[b], cfg)
+            assert_outcome(outs[b], _fields(exp), rtol=TRANS_RTOL, where=f"{mode} q{b}",
+                           exact_bounds=mode != "spherical")
