@@ -1632,6 +1632,10 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
         if (st.mode == MODE_SPARSE) {
             if (lead) DBG_TS(D, 8 + 4 * (st.iter & 3));
             wave_rows<ET, CPL, Q>(D, o, st.p_lo, st.p_hi, hs_w, scratch);
+            if (D.dbg && st.iter == 0) {  // per-CTA end of its rows (before the barrier)
+                __syncthreads();
+                if (threadIdx.x == 0 && blockIdx.x < 128) D.dbg[128 + 512 - 128 + blockIdx.x] = gtimer();
+            }
             grid_sync(D);
             if (lead) DBG_TS(D, 9 + 4 * (st.iter & 3));
             // summaries + scan, chunk by chunk (identical in every CTA)

@@ -45,6 +45,10 @@ for i, h in enumerate(q):
         print(f"CTA starts: first {(st_.min() - t0_) / 1e3:.2f} last {(st_.max() - t0_) / 1e3:.2f} us; "
               f"CTA ends: first {(en_.min() - t0_) / 1e3:.2f} median {(np.median(en_) - t0_) / 1e3:.2f} "
               f"last {(en_.max() - t0_) / 1e3:.2f} us (slowest CTA {int(en_.argmax())})")
+    rw = buf[512:640].astype(np.int64)
+    if rw.any():
+        rw = rw[rw > 0]
+        print(f"rows done per CTA: first {(rw.min() - int(buf[0])) / 1e3:.2f} median {(np.median(rw) - int(buf[0])) / 1e3:.2f} last {(rw.max() - int(buf[0])) / 1e3:.2f} us")
     print(f"head n = {int(buf[63])}")
     buf[63] = 0
     print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} fb={out.fallback_used}")
