@@ -294,12 +294,19 @@ class ShardedDecoder:
         return sums
 
     def _assemble(self, parts, n):
+        """One variable-length all_gather per open: (position, id, logit bits)
+        packed as three int64 columns, so the logits travel bit for bit."""
         pos_l, id_l, lg_l = [], [], []
         for pos, ids, logits, counts in parts:
             mine = len(pos)
-            pos_l += self.comm.all_gather_var(pos.astype(np.int64), mine, counts)
-            id_l += self.comm.all_gather_var(ids.astype(np.int64), mine, counts)
-            lg_l += self.comm.all_gather_var(logits.astype(np.float64), mine, counts)
+            packed = np.stack([pos.astype(np.int64), ids.astype(np.int64),
+                               np.ascontiguousarray(logits, dtype=np.float64).view(np.int64)], axis=1).reshape(-1)
+            got = self.comm.all_gather_var(packed, 3 * mine, [3 * c for c in counts])
+            for g in got:
+                g = g.reshape(-1, 3)
+                pos_l.append(g[:, 0])
+                id_l.append(g[:, 1])
+                lg_l.append(np.ascontiguousarray(g[:, 2]).view(np.float64))
         pos = np.concatenate(pos_l) if pos_l else np.empty(0, np.int64)
         order = np.argsort(pos, kind="stable")
         if pos.size != n or not np.array_equal(pos[order], np.arange(n)):
@@ -352,8 +359,11 @@ class ShardedDecoder:
         tops = np.concatenate([s[SH_TOPK:SH_TOPK + int(s[SH_NLIST])] for s in sums])
         kth = float(-np.sort(-tops)[cfg.k - 1])
         counts = [int(s[SH_NTOK]) for s in sums]
-        all_ids = np.concatenate(self.comm.all_gather_var(ids.astype(np.int64), len(ids), counts))
-        all_lg = np.concatenate(self.comm.all_gather_var(logits.astype(np.float64), len(ids), counts))
+        packed = np.stack([ids.astype(np.int64),
+                           np.ascontiguousarray(logits, dtype=np.float64).view(np.int64)], axis=1).reshape(-1)
+        got = [g.reshape(-1, 2) for g in self.comm.all_gather_var(packed, 2 * len(ids), [2 * c for c in counts])]
+        all_ids = np.concatenate([g[:, 0] for g in got])
+        all_lg = np.concatenate([np.ascontiguousarray(g[:, 1]).view(np.float64) for g in got])
         out = np.empty(self.V, dtype=np.float64)
         out[all_ids] = all_lg
         if all_ids.size != self.V:
