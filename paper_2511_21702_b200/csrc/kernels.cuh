@@ -1093,16 +1093,22 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
     double my_kth = -INFINITY;
     int kc = ss.kcount;
     if (k <= 16) {
-        // sequential merges of 16-entry lists (lane l < 16 holds the l-th largest)
+        // sequential merges of 16-entry lists (lane l < 16 holds the l-th largest).
+        // A cluster whose largest logit does not exceed the current k-th value
+        // cannot change the top-k values (ties add equal values below the cut):
+        // its merge is skipped.
+        double kv = kc >= k ? __shfl_sync(CSVD_FULL, reg_list, k - 1) : -INFINITY;
 #pragma unroll 1
         for (int t = 0; t < q1 - q0; ++t) {
             const int size = o.cum[q0 + t + 1] - o.cum[q0 + t];
             const int kn = size < k ? size : k;
-            const double nv = lane < kn ? c_topk[t * k + lane] : -INFINITY;
-            reg_list = reg_merge16(reg_list, nv, lane);
-            kc = min(k, kc + kn);
-            const double kv = __shfl_sync(CSVD_FULL, reg_list, k - 1);
-            if (lane == t) my_kth = kc >= k ? kv : -INFINITY;
+            if (!(kc >= k && c_max[t] <= kv)) {
+                const double nv = lane < kn ? c_topk[t * k + lane] : -INFINITY;
+                reg_list = reg_merge16(reg_list, nv, lane);
+                kc = min(k, kc + kn);
+                kv = kc >= k ? __shfl_sync(CSVD_FULL, reg_list, k - 1) : -INFINITY;
+            }
+            if (lane == t) my_kth = kv;
         }
     } else {  // k > 16
         double *la = la0, *lb = lb0;
