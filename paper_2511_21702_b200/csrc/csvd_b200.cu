@@ -523,7 +523,9 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemcpy(ctx->d_Uraw_l, ur.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_dots_l, dt.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
         const size_t hsb = sizeof(double) * (size_t)((pw_hs_size(D0.bplan) + 1) & ~1);
-        ctx->kbb_gq = (int)std::min<size_t>(BQN, (227 * 1024) / hsb);
+        ctx->kbb_gq = (int)std::min<size_t>(BQN1, (227 * 1024 - 64) / hsb);
+        if (const char *e = getenv("CSVD_KBB_GQ"))  // queries per pass cap (<= 3: two-cluster path)
+            ctx->kbb_gq = std::max(1, std::min(ctx->kbb_gq, atoi(e)));
         ctx->kbb_smem = hsb * ctx->kbb_gq;
         CK(cudaFuncSetAttribute((const void *)ctx->kbb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ctx->kbb_smem));

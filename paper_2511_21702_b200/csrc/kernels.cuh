@@ -1767,11 +1767,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
 // tree per query as bounds_phase); lanes then start from these bounds.
 // Regular plans only (the bound dimension is d: euclidean / spherical).
 // ---------------------------------------------------------------------------
-#define BQN 3
+#define BQN 3   // queries per register block when a warp pairs two clusters
+#define BQN1 6  // queries per register block at one cluster per warp (C <= warps)
 template <int BQ>
 __global__ void __launch_bounds__(THREADS, 1)
     k_bounds_batch(Dev D, const double *__restrict__ H, int B, double *const *Uraw_l, double *const *dots_l,
-                   csvd_result *res_all, int gq /* queries per pass (<= BQN, by shared memory) */) {
+                   csvd_result *res_all, int gq /* queries per pass (<= BQN1, by shared memory) */) {
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hs_stride = (pw_hs_size(D.bplan) + 1) & ~1;
@@ -1784,20 +1785,40 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int qb = 0; qb < B; qb += gq) {
         const int nq = min(gq, B - qb);
         tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / gq));
-        // two clusters per warp at a time: each staged query value read from
-        // shared memory feeds both rows
-        for (int c = gwarp; c < D.C; c += 2 * nwarps) {
-            const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
-            const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
-            double dots[2][BQN];
-            warp_dot_regular_multi<BQ, BQN, 2>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
-            if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
+        if (D.C <= nwarps && gq > BQN) {
+            // one cluster per warp: the registers a second row would take hold
+            // more queries instead, so fewer passes re-read the centroids
+            const int c = gwarp;
+            if (c < D.C) {
+                const double *const rows[1] = {D.cent + (size_t)c * D.bd};
+                double dots[1][BQN1];
+                warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
+                if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
 #pragma unroll
-                for (int j = 0; j < BQN; ++j)
-                    if (j < nq) {
-                        dots_l[qb + j][c] = dots[0][j];
-                        if (c2 != c) dots_l[qb + j][c2] = dots[1][j];
+                    for (int j = 0; j < BQN1; ++j)
+                        if (j < nq) dots_l[qb + j][c] = dots[0][j];
+                }
+            }
+        } else {
+            // two clusters per warp at a time: each staged query value read
+            // from shared memory feeds both rows
+            for (int j0 = 0; j0 < nq; j0 += BQN) {
+                const int nq2 = min(BQN, nq - j0);
+                for (int c = gwarp; c < D.C; c += 2 * nwarps) {
+                    const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
+                    const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
+                    double dots[2][BQN];
+                    warp_dot_regular_multi<BQ, BQN, 2>(rows, smem + (size_t)j0 * hs_stride, hs_stride, nq2,
+                                                       D.bplan.leaf_len, lane, dots);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < BQN; ++j)
+                            if (j < nq2) {
+                                dots_l[qb + j0 + j][c] = dots[0][j];
+                                if (c2 != c) dots_l[qb + j0 + j][c2] = dots[1][j];
+                            }
                     }
+                }
             }
         }
         __syncthreads();

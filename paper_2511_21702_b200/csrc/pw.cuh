@@ -248,7 +248,9 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&row
                                                        int leaf_len, int lane, double (&out)[NR][NQ]) {
     constexpr int NB = 2;
     const int S = leaf_len >> 3;
-    double slice[NR][NQ][Q];
+    // slice totals combined as they complete, in the (s0+s1)+(s2+s3) tree of
+    // warp_dot_regular: at most two partials per (row, query) stay live
+    double part[NR][NQ], first[NR][NQ];
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
         const double *hp = hs0 + (size_t)(u * 32 + lane) * (leaf_len + 2);
@@ -301,22 +303,19 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&row
                                  d_add(d_add(r[w][j][4], r[w][j][5]), d_add(r[w][j][6], r[w][j][7])));
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
-                slice[w][j][u] = v;
+                if (u % 2 == 0) {
+                    part[w][j] = v;
+                } else {
+                    v = d_add(part[w][j], v);  // s0+s1 or s2+s3
+                    if (u == 1) first[w][j] = v;
+                    else first[w][j] = d_add(first[w][j], v);
+                }
             }
     }
 #pragma unroll
     for (int w = 0; w < NR; ++w)
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-            double tot;
-            if constexpr (Q == 1)
-                tot = slice[w][j][0];
-            else if constexpr (Q == 2)
-                tot = d_add(slice[w][j][0], slice[w][j][1]);
-            else
-                tot = d_add(d_add(slice[w][j][0], slice[w][j][1]), d_add(slice[w][j][2], slice[w][j][3]));
-            out[w][j] = d_add(0.0, tot);
-        }
+        for (int j = 0; j < NQ; ++j) out[w][j] = d_add(0.0, Q == 1 ? part[w][j] : first[w][j]);
 }
 
 // ||h||^2 in the CPL = 8 pairwise order with both operands from the staged

@@ -13,6 +13,9 @@ from paper_2511_21702_b200 import _lib, workload as wl  # noqa: E402
 
 V, d, n_modes, g = 151552, 3584, 2273, 1
 dtype = "bf16"
+if len(sys.argv) > 1 and sys.argv[1] == "c2":  # V=128256 d=4096 C=1024 shape
+    V, d, n_modes, g, dtype = 128256, 4096, 64, 16, "f32"
+    sys.argv.pop(1)
 t0 = time.time()
 T = wl.synth_vocab(V, d, n_modes, 0.3, 1, dtype=dtype)
 ix = wl.fast_index(T, n_modes, g)
