@@ -72,7 +72,8 @@ typedef struct {
     int64_t hidden_dim;       /* d */
     int32_t w_dtype;          /* CSVD_W_F32 | CSVD_W_BF16 */
     const void *weights;      /* [V, d] row-major */
-    const float *bias;        /* [V]  (f32-exact values) */
+    const double *bias;       /* [V]  float64 (any finite values; added to the f64 dot exactly as
+                                 tensor_io.EmbeddingTable holds them) */
 } csvd_table_desc;
 
 /* ClusterIndex stacked arrays (cluster_index.py:96-124), host memory. */
@@ -148,7 +149,7 @@ typedef struct {
 typedef struct csvd_ctx csvd_ctx;
 
 /* Upload a (table, index) pair: permutes W into cluster order on the device,
- * f64 centroids, f32 bias.  Replaces the per-step `_check_table_index`
+ * f64 centroids, f64 bias.  Replaces the per-step `_check_table_index`
  * (decode.py:142-144): the caller verifies the fingerprint once here. */
 int csvd_create(csvd_ctx **out, int device, const csvd_table_desc *table,
                 const csvd_index_desc *index);

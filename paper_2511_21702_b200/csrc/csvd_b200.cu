@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/csvd_b200.h"
-#include "kernels.cuh"
+#include "headstep.cuh"
 
 // permute rows on device: dst[pos] = src[perm[pos]]
 __global__ void k_permute_rows(const char *src, char *dst, const long long *perm, long long V, long long row_bytes) {
@@ -71,18 +71,24 @@ struct csvd_ctx {
     int dense_grid = 0;
     size_t dense_smem = 0;
     int grid = 0;
+    int grid_cap = 0;  // the grid the K-dependent buffers were sized for
     int nsm = 0;
     size_t smem = 0;
     csvd_config *d_cfg = nullptr;
     double *d_h = nullptr;
     double *h_pin = nullptr;
-    csvd_config *cfg_pin = nullptr;
+    // pinned staging configs, one per kind of graph that reads one at execution
+    // time (step/shard: cfg_pin; batch: cfg_pin_b; dense/bounds: cfg_pin_fixed)
+    csvd_config *cfg_pin = nullptr, *cfg_pin_b = nullptr, *cfg_pin_fixed = nullptr;
     csvd_config cfg_dev{};   // the config currently resident in d_cfg
     bool cfg_valid = false;
     csvd_result *res_pin = nullptr;
     long long *ids_pin = nullptr;
     double *logits_pin = nullptr;
     cudaGraphExec_t g_step = nullptr, g_host = nullptr, g_bounds = nullptr, g_dense = nullptr;
+    // head step (headstep.cuh): [h2d] -> k_head -> IF(undecided) k_step
+    void (*khead)(Dev, cudaGraphConditionalHandle) = nullptr;
+    cudaGraphExec_t g_step_head = nullptr, g_host_head = nullptr;
     // zero-copy host results (csvd_step_host): mapped pinned buffers + flag
     csvd_result *res_map = nullptr;
     long long *ids_map = nullptr;
@@ -200,17 +206,44 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
 // --- kernel instantiation per (weight dtype, W plan, bounds plan) ----------
 // (instantiated in kinst.cu, one translation unit per dtype / plan)
 #define CSVD_EXTERN_K(ET, CPL, Q)                                  \
-    extern template __global__ void k_step<ET, CPL, Q, CPL, Q>(Dev); \
-    extern template __global__ void k_step<ET, CPL, Q, 0, 0>(Dev);   \
-    extern template __global__ void k_dense_gemv<ET, CPL, Q>(Dev);   \
-    extern template __global__ void k_step<ET, CPL, Q, CPL, Q, true>(Dev);
+    extern template __global__ void k_step<ET, CPL, Q, CPL, Q>(const __grid_constant__ Dev); \
+    extern template __global__ void k_step<ET, CPL, Q, 0, 0>(const __grid_constant__ Dev);   \
+    extern template __global__ void k_dense_gemv<ET, CPL, Q>(const __grid_constant__ Dev);   \
+    extern template __global__ void k_step<ET, CPL, Q, CPL, Q, true>(const __grid_constant__ Dev);
 #define CSVD_EXTERN_ET(ET) \
     CSVD_EXTERN_K(ET, 8, 1) CSVD_EXTERN_K(ET, 8, 2) CSVD_EXTERN_K(ET, 8, 4) \
     CSVD_EXTERN_K(ET, 4, 1) CSVD_EXTERN_K(ET, 2, 1) CSVD_EXTERN_K(ET, 1, 1)
 CSVD_EXTERN_ET(float)
 CSVD_EXTERN_ET(uint16_t)
-extern template __global__ void k_step<float, 0, 0, 0, 0>(Dev);
-extern template __global__ void k_step<uint16_t, 0, 0, 0, 0>(Dev);
+#define CSVD_EXTERN_HEAD(ET) \
+    extern template __global__ void k_head<ET, 1>(const __grid_constant__ Dev, cudaGraphConditionalHandle); \
+    extern template __global__ void k_head<ET, 2>(const __grid_constant__ Dev, cudaGraphConditionalHandle); \
+    extern template __global__ void k_head<ET, 4>(const __grid_constant__ Dev, cudaGraphConditionalHandle);
+CSVD_EXTERN_HEAD(float)
+CSVD_EXTERN_HEAD(uint16_t)
+typedef void (*khead_t)(Dev, cudaGraphConditionalHandle);
+template <typename ET>
+static khead_t pick_head_t(const PwPlan &wp) {
+    switch (wp.q) {
+        case 1: return k_head<ET, 1>;
+        case 2: return k_head<ET, 2>;
+        default: return k_head<ET, 4>;
+    }
+}
+// the head step needs a regular 8-chain plan shared by W rows and centroids
+// (every d = 32 * 2^m * L with L % 8 == 0; not bias-augmented d + 1)
+static khead_t pick_head(const Dev &D) {
+    if (getenv("CSVD_NO_HEAD")) return nullptr;
+    if (!D.wplan.regular || D.wplan.cpl != 8 || D.wplan.n != D.bplan.n || D.mode == CSVD_MODE_BIAS_AUGMENTED)
+        return nullptr;
+    return D.wdtype == CSVD_W_BF16 ? pick_head_t<uint16_t>(D.wplan) : pick_head_t<float>(D.wplan);
+}
+// configs the head step can decide (everything else goes straight to k_step)
+static bool head_config(const csvd_config *cfg) {
+    return cfg->variant == CSVD_VARIANT_INCREMENTAL && cfg->first_wave_tokens <= 0 && cfg->k <= KH;
+}
+extern template __global__ void k_step<float, 0, 0, 0, 0>(const __grid_constant__ Dev);
+extern template __global__ void k_step<uint16_t, 0, 0, 0, 0>(const __grid_constant__ Dev);
 template <typename ET, int CPL, int Q>
 static kern_t pick_b(bool same) {
     if (same) return k_step<ET, CPL, Q, CPL, Q>;
@@ -264,52 +297,96 @@ static kern_t pick_kernel(const Dev &D) {
     return D.wdtype == CSVD_W_BF16 ? pick_w<uint16_t>(D.wplan, D.bplan) : pick_w<float>(D.wplan, D.bplan);
 }
 
-// shared-memory layout (doubles): hs_w | hs_b? | generic scratch? | ordering | chunk scratch
-static void layout_smem(csvd_ctx *ctx) {
-    Dev &D = ctx->D;
+// shared-memory layout (doubles): hs_w | hs_b? | generic scratch? | ordering | chunk scratch.
+// Pure function of (D, K): the K-dependent part is the chunk scratch (2 running
+// top-k lists + chunk * K cluster lists).  When even chunk = 1 does not fit in
+// 227 KB, those lists move to global memory (per CTA, D.klists): any k <= V
+// is accepted, as in the reference (decode.py:104-115).
+struct SmemPlan {
+    size_t bytes;
+    int hs_off_b, scratch_off, ord_off, sum_off, chunk;
+    bool klists_global;
+};
+static SmemPlan plan_smem(const Dev &D, int K) {
+    SmemPlan p{};
     const bool same = D.wplan.n == D.bplan.n;
     size_t off = pw_hs_size(D.wplan);
     off = (off + 1) & ~(size_t)1;
-    D.hs_off_b = 0;
+    p.hs_off_b = 0;
     if (!same) {
-        D.hs_off_b = (int)off;
+        p.hs_off_b = (int)off;
         off += pw_hs_size(D.bplan);
         off = (off + 1) & ~(size_t)1;
     }
-    D.scratch_off = (int)off;
+    p.scratch_off = (int)off;
     if (!D.wplan.regular || !D.bplan.regular) off += WARPS * (CSVD_MAX_LEAVES / 4);
-    D.ord_off = (int)off;
+    p.ord_off = (int)off;
     // the per-CTA ordering (sort keys, U, Uo, lrh; order, cum)
     off += ord_doubles(D.C, D.Cp);
     off = (off + 1) & ~(size_t)1;
-    D.sum_off = (int)off;
-    // chunk scratch: 9*CHUNK values + 2 K-lists + chunk*K top-k rows
-    const size_t fixed = 9 * CHUNK + 2 * (size_t)D.K;
+    p.sum_off = (int)off;
     const size_t budget = (227 * 1024) / 8;
+    const size_t fixed = 9 * CHUNK;
     int chunk = CHUNK;
-    while (chunk > 1 && off + fixed + (size_t)chunk * D.K > budget) chunk >>= 1;
-    D.chunk = chunk;
-    off += fixed + (size_t)chunk * D.K;
-    ctx->smem = 8 * off;
+    while (chunk > 1 && off + fixed + 2 * (size_t)K + (size_t)chunk * K > budget) chunk >>= 1;
+    if (off + fixed + 2 * (size_t)K + (size_t)chunk * K <= budget) {
+        p.klists_global = false;
+        off += fixed + 2 * (size_t)K + (size_t)chunk * K;
+    } else {
+        p.klists_global = true;  // lists in global memory (L2-resident at these sizes)
+        chunk = CHUNK;
+        off += fixed;
+    }
+    p.chunk = chunk;
+    p.bytes = 8 * off;
+    return p;
+}
+// doubles of global K-list scratch per CTA (klists_global plans)
+static size_t klist_stride(const SmemPlan &p, int K) { return 2 * (size_t)K + (size_t)p.chunk * K; }
+
+static void layout_smem(csvd_ctx *ctx) {
+    Dev &D = ctx->D;
+    const SmemPlan p = plan_smem(D, D.K);
+    D.hs_off_b = p.hs_off_b;
+    D.scratch_off = p.scratch_off;
+    D.ord_off = p.ord_off;
+    D.sum_off = p.sum_off;
+    D.chunk = p.chunk;
+    ctx->smem = p.bytes;
 }
 
+// K-dependent device buffers: dense candidate lists [grid*WARPS, K], the shard
+// aggregate, and (large K) the per-CTA global K-lists.  Allocated into
+// temporaries first: on failure the context keeps its previous, consistent K.
 static int alloc_k(csvd_ctx *ctx, int K) {
     Dev &D = ctx->D;
+    const SmemPlan pl = plan_smem(D, K);
+    // per-CTA / per-warp buffers are sized for the current grid, which is then
+    // a cap: configure() never grows the grid past it (a smaller plan for a new
+    // K could otherwise raise the occupancy above what the buffers hold)
+    const int grid = ctx->grid;
+    void *nb[4] = {};
+    const size_t sizes[3] = {sizeof(double) * (size_t)grid * WARPS * K + 16,
+                             sizeof(double) * (CSVD_SH_TOPK + (size_t)K) + 16,
+                             pl.klists_global ? sizeof(double) * (size_t)grid * klist_stride(pl, K) + 16 : 0};
+    for (int i = 0; i < 3; ++i) {
+        if (!sizes[i]) continue;
+        cudaError_t e = cudaMalloc(&nb[i], sizes[i]);
+        if (e != cudaSuccess) {
+            for (int j = 0; j < i; ++j)
+                if (nb[j]) cudaFree(nb[j]);
+            return fail(ctx, CSVD_ENOMEM, std::string("cudaMalloc (k workspace): ") + cudaGetErrorString(e));
+        }
+    }
     for (int i = 0; i < 4; ++i)
         if (ctx->k_buffers[i]) cudaFree(ctx->k_buffers[i]);
-    memset(ctx->k_buffers, 0, sizeof(ctx->k_buffers));
-    const size_t nw = (size_t)ctx->grid * WARPS;
-    void *p;
-    CK(cudaMalloc(&p, sizeof(double) * nw * K + 16));
-    ctx->k_buffers[0] = p;
-    D.cand = (double *)p;
-    CK(cudaMalloc(&p, sizeof(double) * (size_t)D.C * K + 16));
-    ctx->k_buffers[1] = p;
-    D.sum_topk = (double *)p;
-    CK(cudaMalloc(&p, sizeof(double) * (CSVD_SH_TOPK + (size_t)K) + 16));
-    ctx->k_buffers[2] = p;
-    D.shard_out = (double *)p;
+    for (int i = 0; i < 4; ++i) ctx->k_buffers[i] = nb[i];
+    D.cand = (double *)nb[0];
+    D.shard_out = (double *)nb[1];
+    D.klists = (double *)nb[2];
+    D.klist_stride = pl.klists_global ? klist_stride(pl, K) : 0;
     D.K = K;
+    ctx->grid_cap = grid;
     return 0;
 }
 
@@ -324,8 +401,16 @@ static int configure(csvd_ctx *ctx) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kern, THREADS, ctx->smem));
     if (occ < 1) return fail(ctx, CSVD_ECONFIG, "step kernel does not fit on an SM");
     ctx->grid = ctx->nsm * occ;
+    if (ctx->grid_cap > 0 && ctx->grid > ctx->grid_cap) ctx->grid = ctx->grid_cap;
     D.nblocks = ctx->grid;
     ctx->kdense = getenv("CSVD_DENSE_PERSISTENT") ? nullptr : pick_dense(D);
+    ctx->khead = ctx->shard ? nullptr : pick_head(D);
+    if (ctx->khead) {
+        CK(cudaFuncSetAttribute((const void *)ctx->khead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+        int occh = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occh, ctx->khead, THREADS, ctx->smem));
+        if (occh * ctx->nsm < ctx->grid) ctx->khead = nullptr;  // must co-reside like k_step
+    }
     // L2 bulk prefetch policy (measured: prefetching rows ahead in the dense GEMV
     // causes re-reads and costs 25%; CSVD_DENSE_PD / CSVD_PF override)
     D.dense_pd = getenv("CSVD_DENSE_PD") ? atoi(getenv("CSVD_DENSE_PD")) : 0;
@@ -364,7 +449,7 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
     // step graphs carry no config upload: the config is uploaded only when it
     // changes (sync_cfg), so an unchanged config costs no copy node per step
     if (mode != LAUNCH_STEP)
-        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin_fixed, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     // host I/O: the kernel itself writes the result into mapped host memory
     int rc = launch(ctx, mode, s, host_io);
     if (rc) {
@@ -374,6 +459,59 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
     CK(cudaStreamEndCapture(s, &g));
     CK(cudaGraphInstantiate(out, g, 0));
     CK(cudaGraphDestroy(g));
+    return 0;
+}
+
+// [h2d h] -> k_head -> IF(handle) { k_step }: the handle defaults to 1 every
+// replay; k_head sets it to 0 once it has decided the step.
+static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
+    cudaStream_t s = ctx->stream;
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
+    Dev D = host_io ? ctx->Dhost : ctx->D;
+    D.launch_mode = LAUNCH_STEP;
+    void *args[] = {&D, &h};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)ctx->khead, dim3(ctx->grid), dim3(THREADS), args,
+                                                ctx->smem, s);
+    cudaGraph_t g2;
+    cudaError_t e2 = cudaStreamEndCapture(s, &g2);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(ctx, CSVD_ECUDA, std::string("head graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+    }
+    // the leaf (k_head) node
+    size_t n = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(g, nodes.data(), &n));
+    cudaGraphNode_t leaf = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+        size_t nd_out = 0;
+        CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out));
+        if (nd_out == 0) leaf = nd;
+    }
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CK(cudaGraphAddNode(&cn, g, &leaf, 1, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    int rc = launch(ctx, LAUNCH_STEP, s, host_io);
+    e2 = cudaStreamEndCapture(s, &g2);
+    if (rc || e2 != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return rc ? rc : fail(ctx, CSVD_ECUDA, std::string("head graph body: ") + cudaGetErrorString(e2));
+    }
+    e = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("head graph instantiate: ") + cudaGetErrorString(e));
     return 0;
 }
 
@@ -389,7 +527,8 @@ static int build_graphs(csvd_ctx *ctx) {
         CK(cudaHostGetDevicePointer(&p, ctx->logits_map, 0));
         H.logits_host = (double *)p;
     }
-    for (cudaGraphExec_t *g : {&ctx->g_step, &ctx->g_host, &ctx->g_bounds, &ctx->g_dense}) {
+    for (cudaGraphExec_t *g : {&ctx->g_step, &ctx->g_host, &ctx->g_bounds, &ctx->g_dense, &ctx->g_step_head,
+                               &ctx->g_host_head}) {
         if (*g) cudaGraphExecDestroy(*g);
         *g = nullptr;
     }
@@ -398,12 +537,17 @@ static int build_graphs(csvd_ctx *ctx) {
         if ((rc = capture(ctx, LAUNCH_STEP, false, &ctx->g_step))) return rc;
         if ((rc = capture(ctx, LAUNCH_STEP, true, &ctx->g_host))) return rc;
         if ((rc = capture(ctx, LAUNCH_DENSE, false, &ctx->g_dense))) return rc;
+        if (ctx->khead) {
+            if ((rc = capture_head(ctx, false, &ctx->g_step_head))) return rc;
+            if ((rc = capture_head(ctx, true, &ctx->g_host_head))) return rc;
+        }
     }
     if ((rc = capture(ctx, LAUNCH_BOUNDS, false, &ctx->g_bounds))) return rc;
     return 0;
 }
 
 static int check_cfg(csvd_ctx *ctx, const csvd_config *cfg);
+static void fixed_cfg(csvd_config *cfg, long long V, int slack_f32);
 
 static void free_lanes(csvd_ctx *ctx) {
     if (ctx->g_batch) cudaGraphExecDestroy(ctx->g_batch);
@@ -469,16 +613,17 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         Dev L = D0;  // shared read-only table / index data, own workspaces
         L.h = ctx->d_H + (size_t)b * D0.d;
         L.res = ctx->d_res_all + b;
+        const SmemPlan pl = plan_smem(D0, K);
+        L.klists = nullptr;
+        L.klist_stride = pl.klists_global ? klist_stride(pl, K) : 0;
         if ((rc = lalloc(ctx, &L.U, C)) || (rc = lalloc(ctx, &L.Uraw, C)) || (rc = lalloc(ctx, &L.dots, C)) ||
-            (rc = lalloc(ctx, &L.cnt, C)) || (rc = lalloc(ctx, &L.order_g, C)) ||
-            (rc = lalloc(ctx, &L.cum_g, C + 1)) || (rc = lalloc(ctx, &L.sum_lse, C)) ||
-            (rc = lalloc(ctx, &L.sum_min, C)) || (rc = lalloc(ctx, &L.sum_max, C)) ||
+            (rc = lalloc(ctx, &L.order_g, C)) || (rc = lalloc(ctx, &L.cum_g, C + 1)) ||
             (rc = lalloc(ctx, &L.S_logits, (size_t)V)) || (rc = lalloc(ctx, &L.S_ids, (size_t)V)) ||
             (rc = lalloc(ctx, &L.st, 1)) || (rc = lalloc(ctx, &L.bar, 4)) ||
-            (rc = lalloc(ctx, &L.cand, (size_t)G * WARPS * K)) || (rc = lalloc(ctx, &L.sum_topk, (size_t)C * K)) ||
-            (rc = lalloc(ctx, &L.shard_out, (size_t)CSVD_SH_TOPK + K)))
+            (rc = lalloc(ctx, &L.cand, (size_t)G * WARPS * K)) ||
+            (rc = lalloc(ctx, &L.shard_out, (size_t)CSVD_SH_TOPK + K)) ||
+            (pl.klists_global && (rc = lalloc(ctx, &L.klists, (size_t)G * L.klist_stride))))
             return rc;
-        CK(cudaMemset(L.cnt, 0, sizeof(int) * C));
         CK(cudaMemset(L.bar, 0, 16));
         CK(cudaMemset(L.st, 0, sizeof(ScanState)));
         L.nblocks = G;
@@ -537,19 +682,15 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             w.U = L.U;
             w.Uraw = L.Uraw;
             w.dots = L.dots;
-            w.cnt = L.cnt;
             w.order_g = L.order_g;
             w.cum_g = L.cum_g;
-            w.sum_lse = L.sum_lse;
-            w.sum_min = L.sum_min;
-            w.sum_max = L.sum_max;
             w.S_logits = L.S_logits;
             w.S_ids = L.S_ids;
             w.st = L.st;
             w.res = L.res;
             w.bar = L.bar;
             w.cand = L.cand;
-            w.sum_topk = L.sum_topk;
+            w.klists = L.klists;
             w.shard_out = L.shard_out;
             w.res_host = L.res_host;
             w.ids_host = L.ids_host;
@@ -588,7 +729,7 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     if (host_io)
         CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin_b, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
         ctx->kbb<<<ctx->grid, THREADS, ctx->kbb_smem, s>>>(D0, ctx->d_H, B, ctx->d_Uraw_l, ctx->d_dots_l,
                                                            ctx->d_res_all, ctx->kbb_gq);
@@ -628,13 +769,24 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     return 0;
 }
 
-static int batch_prepare(csvd_ctx *ctx, int B, const csvd_config *cfg, bool host_io) {
+// Rewrite a pinned staging config that queued graphs' memcpy nodes read at
+// execution time: wait for the streams first when the contents change (an
+// earlier asynchronous replay must still see the config it was issued with).
+static int stage_pinned_cfg(csvd_ctx *ctx, csvd_config *pin, const csvd_config &cfg, cudaStream_t s) {
+    if (memcmp(pin, &cfg, sizeof cfg) == 0) return 0;
+    CK(cudaStreamSynchronize(s));
+    if (s != ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+    *pin = cfg;
+    return 0;
+}
+
+static int batch_prepare(csvd_ctx *ctx, int B, const csvd_config *cfg, bool host_io, cudaStream_t s) {
     if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (B < 1 || B > 1024) return fail(ctx, CSVD_ECONFIG, "batch size must be in [1, 1024]");
     int rc = check_cfg(ctx, cfg);
     if (rc) return rc;
     if ((rc = ensure_lanes(ctx, B))) return rc;
-    *ctx->cfg_pin = *cfg;
+    if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin_b, *cfg, s))) return rc;
     if (!ctx->g_batch || ctx->g_batch_B != B || ctx->g_batch_host != (host_io ? 1 : 0))
         if ((rc = capture_batch(ctx, B, host_io))) return rc;
     return 0;
@@ -644,9 +796,9 @@ extern "C" int csvd_step_batch_device(csvd_ctx *ctx, int32_t B, const double *H_
                                       void *stream) {
     if (!ctx || !cfg || !H_dev) return CSVD_ESTATE;
     CK(cudaSetDevice(ctx->device));
-    int rc = batch_prepare(ctx, B, cfg, false);
-    if (rc) return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+    int rc = batch_prepare(ctx, B, cfg, false, s);
+    if (rc) return rc;
     if (H_dev != ctx->d_H)
         CK(cudaMemcpyAsync(ctx->d_H, H_dev, sizeof(double) * B * ctx->D.d, cudaMemcpyDeviceToDevice, s));
     CK(cudaGraphLaunch(ctx->g_batch, s));
@@ -657,9 +809,9 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
                                     csvd_result *res, int64_t *ids, double *logits, int64_t cap) {
     if (!ctx || !cfg || !H || !res) return CSVD_ESTATE;
     CK(cudaSetDevice(ctx->device));
-    int rc = batch_prepare(ctx, B, cfg, true);
-    if (rc) return rc;
     cudaStream_t s = ctx->stream;
+    int rc = batch_prepare(ctx, B, cfg, true, s);
+    if (rc) return rc;
     static const bool prof = getenv("CSVD_PROFILE_HOST") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto t0 = now();
@@ -685,7 +837,6 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
         CK(cudaMemset(ctx->d_res_all, 0, sizeof(csvd_result) * B));
         for (Lane &l : ctx->lanes) {
             CK(cudaMemset(l.D.bar, 0, 16));
-            CK(cudaMemset(l.D.cnt, 0, sizeof(int) * ctx->D.C));
         }
         if (value_err) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
         return fail(ctx, CSVD_ESTATE, "device state error in a batch lane (grid barrier timeout)");
@@ -722,15 +873,24 @@ extern "C" int csvd_batch_lanes(csvd_ctx *ctx, int32_t *lanes, int32_t *grid_per
 extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
     if (!ctx) return CSVD_ESTATE;
     if (k <= ctx->D.K) return 0;
+    if (k < 1 || (long long)k > (long long)ctx->D.V) return fail(ctx, CSVD_ECONFIG, "need 1 <= k <= V");
     int K = 32;
     while (K < k) K <<= 1;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // queued graphs still reference the old buffers
     int rc;
     free_lanes(ctx);  // lanes are rebuilt for the new K on the next batch
-    if ((rc = alloc_k(ctx, K))) return rc;
-    if ((rc = configure(ctx))) return rc;
-    return build_graphs(ctx);
+    if ((rc = alloc_k(ctx, K))) return rc;  // all-or-nothing: the old K stays valid on failure
+    if ((rc = configure(ctx)) || (rc = build_graphs(ctx))) {
+        // no graph may keep pointing at buffers of a half-applied K
+        for (cudaGraphExec_t *g : {&ctx->g_step, &ctx->g_host, &ctx->g_bounds, &ctx->g_dense, &ctx->g_step_head,
+                                   &ctx->g_host_head}) {
+            if (*g) cudaGraphExecDestroy(*g);
+            *g = nullptr;
+        }
+        return rc;
+    }
+    return 0;
 }
 
 static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, const csvd_index_desc *ix,
@@ -845,15 +1005,15 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
             D.lpos = dw;
         }
     }
-    std::vector<float> biasp(V);
+    std::vector<double> biasp(V);
     std::vector<int> perm32(V);
     for (long long p = 0; p < V; ++p) {
         long long tok = ix->perm[p];
         if (tok < 0 || tok >= V) return fail(ctx, CSVD_ECONFIG, "perm out of range");
         perm32[p] = (int)tok;
-        biasp[p] = t->bias ? t->bias[tok] : 0.0f;
+        biasp[p] = t->bias ? t->bias[tok] : 0.0;
     }
-    float *dbias;
+    double *dbias;
     int *dperm;
     if ((rc = dupload(ctx, &dbias, biasp.data(), (size_t)V))) return rc;
     if ((rc = dupload(ctx, &dperm, perm32.data(), (size_t)V))) return rc;
@@ -910,19 +1070,19 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     if ((rc = dalloc(ctx, &D.U, C))) return rc;
     if ((rc = dalloc(ctx, &D.dots, C))) return rc;
     if ((rc = dalloc(ctx, &D.Uraw, C))) return rc;
-    if ((rc = dalloc(ctx, &D.cnt, C))) return rc;
-    CK(cudaMemset(D.cnt, 0, sizeof(int) * C));
     if ((rc = dalloc(ctx, &D.order_g, C))) return rc;
     if ((rc = dalloc(ctx, &D.cum_g, C + 1))) return rc;
-    if ((rc = dalloc(ctx, &D.sum_lse, C))) return rc;
-    if ((rc = dalloc(ctx, &D.sum_min, C))) return rc;
-    if ((rc = dalloc(ctx, &D.sum_max, C))) return rc;
     if ((rc = dalloc(ctx, &D.S_logits, (size_t)V))) return rc;
     if ((rc = dalloc(ctx, &D.S_ids, (size_t)V))) return rc;
     if ((rc = dalloc(ctx, &D.st, 1))) return rc;
     if ((rc = dalloc(ctx, &D.res, 1))) return rc;
     if ((rc = dalloc(ctx, &D.bar, 4))) return rc;
     CK(cudaMemset(D.bar, 0, 16));
+    if ((rc = dalloc(ctx, &D.hws, (size_t)HMAX * (3 + KH)))) return rc;
+    if ((rc = dalloc(ctx, &D.hcnt, (size_t)HMAX + 1))) return rc;
+    CK(cudaMemset(D.hcnt, 0, sizeof(int) * (HMAX + 1)));
+    if ((rc = dalloc(ctx, &D.bar64, 2))) return rc;
+    CK(cudaMemset(D.bar64, 0, 16));
     CK(cudaMemset(D.st, 0, sizeof(ScanState)));
     CK(cudaMemset(D.res, 0, sizeof(csvd_result)));
     D.dbg = nullptr;
@@ -937,6 +1097,10 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     ctx->first_chunk = D.V < 4096 ? D.V : 4096;
     CK(cudaHostAlloc(&ctx->h_pin, sizeof(double) * (D.d + 1), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->cfg_pin, sizeof(csvd_config), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->cfg_pin_b, sizeof(csvd_config), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->cfg_pin_fixed, sizeof(csvd_config), cudaHostAllocDefault));
+    memset(ctx->cfg_pin_b, 0, sizeof(csvd_config));
+    fixed_cfg(ctx->cfg_pin_fixed, D.V, 0);
     CK(cudaHostAlloc(&ctx->res_pin, sizeof(csvd_result), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->ids_pin, sizeof(long long) * V, cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->logits_pin, sizeof(double) * V, cudaHostAllocDefault));
@@ -948,7 +1112,7 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     D.ids_host = nullptr;
     D.logits_host = nullptr;
     D.K = 32;
-    if ((rc = configure(ctx))) return rc;
+    if ((rc = configure(ctx))) return rc;  // grid size first (K buffers are per CTA / warp)
     if ((rc = alloc_k(ctx, 32))) return rc;
     if ((rc = configure(ctx))) return rc;
     return build_graphs(ctx);
@@ -968,7 +1132,7 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     if (!ctx) return 0;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (cudaGraphExec_t g : {ctx->g_step, ctx->g_host, ctx->g_bounds, ctx->g_dense})
+    for (cudaGraphExec_t g : {ctx->g_step, ctx->g_host, ctx->g_bounds, ctx->g_dense, ctx->g_step_head, ctx->g_host_head})
         if (g) cudaGraphExecDestroy(g);
     free_lanes(ctx);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -977,7 +1141,8 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
         if (ctx->k_buffers[i]) cudaFree(ctx->k_buffers[i]);
     if (ctx->flush_buf) cudaFree(ctx->flush_buf);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
-    if (ctx->cfg_pin) cudaFreeHost(ctx->cfg_pin);
+    for (csvd_config *p : {ctx->cfg_pin, ctx->cfg_pin_b, ctx->cfg_pin_fixed})
+        if (p) cudaFreeHost(p);
     if (ctx->res_pin) cudaFreeHost(ctx->res_pin);
     if (ctx->ids_pin) cudaFreeHost(ctx->ids_pin);
     if (ctx->logits_pin) cudaFreeHost(ctx->logits_pin);
@@ -1009,7 +1174,8 @@ static int result_error(csvd_ctx *ctx, const csvd_result &r) {
     cudaMemset(&ctx->D.res->error, 0, sizeof(int32_t));
     if (r.error == CSVD_EVALUE) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
     cudaMemset(ctx->D.bar, 0, 16);  // a timed-out barrier leaves stale counts
-    cudaMemset(ctx->D.cnt, 0, sizeof(int) * ctx->D.C);
+    cudaMemset(ctx->D.bar64, 0, 16);
+    cudaMemset(ctx->D.hcnt, 0, sizeof(int) * (HMAX + 1));
     return fail(ctx, r.error, "device state error (grid barrier timeout)");
 }
 
@@ -1037,7 +1203,9 @@ extern "C" int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_c
         CK(cudaMemcpyAsync(ctx->d_h, h_dev, sizeof(double) * ctx->D.d, cudaMemcpyDeviceToDevice, s));
     if ((rc = sync_cfg(ctx, cfg, s))) return rc;
     if (ctx->direct) return launch(ctx, LAUNCH_STEP, s);
-    CK(cudaGraphLaunch(ctx->g_step, s));
+    cudaGraphExec_t g = (ctx->g_step_head && head_config(cfg)) ? ctx->g_step_head : ctx->g_step;
+    if (!g) return fail(ctx, CSVD_ESTATE, "no step graph (an earlier workspace change failed)");
+    CK(cudaGraphLaunch(g, s));
     return 0;
 }
 
@@ -1073,7 +1241,9 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         static const bool prof = getenv("CSVD_PROFILE_HOST") != nullptr;
         auto t1 = std::chrono::steady_clock::now();
         ctx->res_map->kind = CSVD_KIND_NONE - 1;  // sentinel: overwritten by the kernel
-        CK(cudaGraphLaunch(ctx->g_host, s));
+        cudaGraphExec_t g = (ctx->g_host_head && head_config(cfg)) ? ctx->g_host_head : ctx->g_host;
+        if (!g) return fail(ctx, CSVD_ESTATE, "no step graph (an earlier workspace change failed)");
+        CK(cudaGraphLaunch(g, s));
         auto t2 = std::chrono::steady_clock::now();
         cudaError_t q;
         while ((q = cudaStreamQuery(s)) == cudaErrorNotReady) {
@@ -1134,12 +1304,14 @@ extern "C" int csvd_bounds_host(csvd_ctx *ctx, const double *h, int32_t slack_f3
     if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    fixed_cfg(ctx->cfg_pin, ctx->D.V, slack_f32);
+    csvd_config fc;
+    fixed_cfg(&fc, ctx->D.V, slack_f32);
+    int rc;
+    if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin_fixed, fc, s))) return rc;
     memcpy(ctx->h_pin, h, sizeof(double) * ctx->D.d);
     CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
-    int rc;
     if (ctx->direct) {
-        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin_fixed, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
         if ((rc = launch(ctx, LAUNCH_BOUNDS, s))) return rc;
     } else {
         CK(cudaGraphLaunch(ctx->g_bounds, s));
@@ -1155,9 +1327,12 @@ extern "C" int csvd_bounds_host(csvd_ctx *ctx, const double *h, int32_t slack_f3
 static int dense_async(csvd_ctx *ctx, cudaStream_t s) {
     if (ctx) ctx->cfg_valid = false;  // this path writes its own config into d_cfg
     if (!ctx->D.W) return fail(ctx, CSVD_ECONFIG, "bounds-only context (no table)");
-    fixed_cfg(ctx->cfg_pin, ctx->D.V, 0);
+    csvd_config fc;
+    fixed_cfg(&fc, ctx->D.V, 0);
+    int rc;
+    if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin_fixed, fc, s))) return rc;
     if (ctx->direct) {
-        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin_fixed, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
         return launch(ctx, LAUNCH_DENSE, s);
     }
     CK(cudaGraphLaunch(ctx->g_dense, s));
@@ -1203,7 +1378,7 @@ extern "C" int csvd_shard_open(csvd_ctx *ctx, const double *h, const csvd_config
     if (cfg->variant != CSVD_VARIANT_BATCHSELECT) return fail(ctx, CSVD_ECONFIG, "shard opens use batch-select order");
     const Dev &D = ctx->D;
     memcpy(ctx->h_pin, h, sizeof(double) * D.d);
-    *ctx->cfg_pin = *cfg;
+    if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin, *cfg, s))) return rc;
     CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * D.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
     if ((rc = launch(ctx, LAUNCH_SHARD, s))) return rc;
@@ -1258,8 +1433,12 @@ extern "C" int csvd_shard_dense(csvd_ctx *ctx, const double *h, int32_t k, doubl
     int rc;
     if (k > D0.K && (rc = csvd_reserve_k(ctx, k))) return rc;
     const Dev &D = ctx->D;
-    fixed_cfg(ctx->cfg_pin, D.V, 0);
-    ctx->cfg_pin->k = k;
+    {
+        csvd_config fc;
+        fixed_cfg(&fc, D.V, 0);
+        fc.k = k;
+        if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin, fc, s))) return rc;
+    }
     memcpy(ctx->h_pin, h, sizeof(double) * D.d);
     CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * D.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin, sizeof(csvd_config), cudaMemcpyHostToDevice, s));

@@ -49,13 +49,13 @@ enum { LAUNCH_STEP = 0, LAUNCH_BOUNDS = 1, LAUNCH_DENSE = 2, LAUNCH_SHARD = 3 };
 struct LaneWS {
     const double *h;
     double *U, *Uraw, *dots;
-    int *cnt, *order_g, *cum_g;
-    double *sum_lse, *sum_min, *sum_max, *S_logits;
+    int *order_g, *cum_g;
+    double *S_logits;
     long long *S_ids;
     ScanState *st;
     csvd_result *res;
     unsigned *bar;
-    double *cand, *sum_topk, *shard_out;
+    double *cand, *klists, *shard_out;
     csvd_result *res_host;
     long long *ids_host;
     double *logits_host;
@@ -65,7 +65,7 @@ struct Dev {
     int V, d, C, Cp, bd, mode, wdtype;  // Cp: C rounded up to a power of two (sort)
     int K;  // top-k capacity (row stride of the dense candidate lists, list buffers)
     const void *W;      // [V, d] permuted rows (fp32 | bf16)
-    const float *bias;  // [V] permuted
+    const double *bias; // [V] permuted, f64 (EmbeddingTable.bias, tensor_io.py:69-94)
     const int *perm;    // [V] position -> token id
     const double *cent; // [C, bd]
     const double *radii, *maxb, *cnorm, *ang, *maxn, *minn, *logsz, *meanb;
@@ -89,9 +89,8 @@ struct Dev {
     const double *h;         // [d]
     const csvd_config *cfg;
     double *U, *Uraw, *dots; // [C] by cluster id (U final with slack; Uraw / dots from the bounds phase)
-    int *cnt;                // [C] rows finished per opening position (reset by the summariser)
-    double *sum_topk;        // [C*K] per-position cluster top-k (desc), from the rows phase
-    double *sum_lse, *sum_min, *sum_max;  // [C]
+    double *klists;          // null, or per-CTA global K-lists (k too large for shared memory)
+    size_t klist_stride;     // doubles per CTA in klists
     double *S_logits;        // [V]
     long long *S_ids;        // [V]
     double *cand;            // [nwarps*K] dense per-warp candidates
@@ -110,6 +109,11 @@ struct Dev {
     int sum_off;             // chunk summaries + scan scratch
     int chunk;               // clusters per summary/scan chunk (<= CHUNK)
     unsigned long long *dbg; // optional phase timestamps (CSVD_DEBUG_TS)
+    // head kernel (headstep.cuh): cluster summaries [3*HMAX + HMAX*KH], row /
+    // cluster completion counters [HMAX + 1], monotone grid-barrier counter
+    double *hws;
+    int *hcnt;
+    unsigned long long *bar64;
 };
 
 // this CTA's index / the CTA count of its step's grid: the whole launch, or
@@ -310,7 +314,7 @@ __device__ __forceinline__ double row_logit(const Dev &D, int wrow, int pos, con
                                             int lane) {
     const ET *row = reinterpret_cast<const ET *>(D.W) + (size_t)wrow * D.d;
     double dot = warp_dot_t<ET, CPL, Q>(row, hs, D.wplan, scratch, lane);
-    return __dadd_rn(dot, (double)__ldg(D.bias + pos));
+    return __dadd_rn(dot, __ldg(D.bias + pos));
 }
 
 // ---------------------------------------------------------------------------
@@ -432,7 +436,8 @@ __device__ __forceinline__ double block_max(double v, double *red) {
 // Stage U + slack (bounds.py:58-64, which needs max |U| first) by cluster id
 // in shared memory; CTA 0 publishes it for cluster_bounds (bounds.py:178-184).
 // Returns false (in every CTA) if a bound is non-finite.
-static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, double qn_given) {
+static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, double qn_given,
+                                                    double *eta_out = nullptr) {
     const int tid = threadIdx.x;
     const int C = D.C;
     const csvd_config &cfg = *D.cfg;
@@ -479,6 +484,7 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, 
         xs[c] = __dadd_rn(xs[c], u);  // certify.py:119 np.log(sizes) + U
         if (CTA_ID == 0) D.U[c] = u;
     }
+    if (eta_out && tid == 0) *eta_out = eta;
     bad = __syncthreads_or(bad);
     if (CTA_ID == 0 && tid == 0) D.res->slack = eta;
     return !bad;
@@ -1439,7 +1445,8 @@ __device__ void shard_open(const Dev &D, const Ord &o, ScanShared &ss, const dou
     grid_sync(D);
     if (CTA_ID != 0) return;
     double *c_lse = sws, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
-    double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
+    double *la = D.klists ? D.klists + (size_t)CTA_ID * D.klist_stride : c_max + CHUNK;
+    double *lb = la + D.K, *c_topk = lb + D.K;
     __shared__ int s_own[CHUNK];
     double reg_list = -INFINITY, m = -INFINITY, ssum = 0.0, mn = INFINITY, mx = -INFINITY;
     int kc = 0, ntok = 0;
@@ -1630,7 +1637,9 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
     }
     // chunk scratch: [6*CHUNK values][CHUNK lse][CHUNK min][CHUNK max][2 K-lists][chunk*k topk]
     double *c_vals = sws, *c_lse = sws + 6 * CHUNK, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
-    double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
+    // the K-lists: shared memory, or this CTA's slice of D.klists (large k)
+    double *la = D.klists ? D.klists + (size_t)CTA_ID * D.klist_stride : c_max + CHUNK;
+    double *lb = la + D.K, *c_topk = lb + D.K;
     double reg_list = -INFINITY;
     for (int guard = 0; guard < D.C + 8; ++guard) {
         const ScanState st = ss.st;
@@ -1725,7 +1734,7 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
 }
 
 template <typename ET, int CPL, int Q, int BCPL, int BQ, bool GROUPED = false>
-__global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
+__global__ void __launch_bounds__(THREADS, 1) k_step(const __grid_constant__ Dev D0) {
     if constexpr (GROUPED) {
         // one launch runs a whole batch: lane b is blockIdx.x / nblocks and
         // swaps its own workspaces into the Dev (all table data is shared)
@@ -1735,19 +1744,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(Dev D0) {
         D.U = w.U;
         D.Uraw = w.Uraw;
         D.dots = w.dots;
-        D.cnt = w.cnt;
         D.order_g = w.order_g;
         D.cum_g = w.cum_g;
-        D.sum_lse = w.sum_lse;
-        D.sum_min = w.sum_min;
-        D.sum_max = w.sum_max;
         D.S_logits = w.S_logits;
         D.S_ids = w.S_ids;
         D.st = w.st;
         D.res = w.res;
         D.bar = w.bar;
         D.cand = w.cand;
-        D.sum_topk = w.sum_topk;
+        D.klists = w.klists;
         D.shard_out = w.shard_out;
         D.res_host = w.res_host;
         D.ids_host = w.ids_host;
@@ -1832,7 +1837,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // logits scattered to token order.  Regular plans only.
 // ---------------------------------------------------------------------------
 template <typename ET, int CPL, int Q>
-__global__ void __launch_bounds__(THREADS, 2) k_dense_gemv(Dev D) {
+__global__ void __launch_bounds__(THREADS, 2) k_dense_gemv(const __grid_constant__ Dev D) {
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pw_stage<CPL>(D.wplan, D.h, D.d, smem, D.wsrc);

@@ -60,7 +60,7 @@ class DeviceIndex:
     """A (table, index) pair resident on one B200 (the `prepare` step).
 
     Layout in HBM: W permuted to cluster order (each cluster a contiguous row
-    range, fp32 or bf16), bias permuted (f32), f64 centroids, per-cluster
+    range, fp32 or bf16), bias permuted (f64), f64 centroids, per-cluster
     radius / max-bias / log-size, and static per-step workspaces sized for the
     worst case (|S| <= V).  See DESIGN.md §3.
     """
@@ -103,8 +103,8 @@ class DeviceIndex:
                     raise ValueError("float64 weights must be float32-exact (tensor_io.py:156)")
                 wa = c(wa, np.float32)
             td.weights = wa.ctypes.data
-            b32 = c(np.asarray(table.bias, dtype=np.float32), np.float32)
-            td.bias = b32.ctypes.data
+            b64 = c(np.asarray(table.bias, dtype=np.float64), np.float64)  # exact: logit = dot + b
+            td.bias = b64.ctypes.data
             self.w_dtype = "bf16" if td.w_dtype == _lib.W_BF16 else "f32"
         else:
             td.w_dtype = _lib.W_F32

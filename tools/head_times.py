@@ -1,0 +1,43 @@
+"""Debug: per-phase device timestamps of the head step (CSVD_DEBUG_TS=1)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+os.environ["CSVD_DEBUG_TS"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_21702_b200 as P  # noqa: E402
+from paper_2511_21702_b200 import _lib, workload as wl  # noqa: E402
+
+V, d, C, g = [int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (128256, 4096, 1024, 16))]
+dtype = os.environ.get("DTYPE", "f32")
+T = wl.synth_vocab(V, d, C // g, 0.3, 1, dtype=dtype)
+ix = wl.fast_index(T, C // g, g)
+q = wl.generate_queries(12, d, "contextual", 7, centroids=ix.centroids)
+ctx = P.prepare(T, ix)
+lib = _lib.load()
+lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+cfg = P.DecodeConfig(k=10)
+names = {24: "kernel start", 25: "h staged", 26: "cta0 bounds done", 27: "barrier passed", 28: "head done (cta0)",
+         29: "scanner start", 30: "scan done"}
+for i, h in enumerate(q):
+    buf = np.zeros(128 + 512, dtype=np.uint64)
+    if not os.environ.get("NOFLUSH"):
+        lib.csvd_l2_flush(ctx._ctx, None)
+    out = ctx.step(h, ctx.make_config(cfg))
+    lib.csvd_debug_timestamps(ctx._ctx, buf.ctypes.data)
+    if i < 2:
+        continue
+    t0 = int(buf[24])
+    nb = ctx.info()["grid_ctas"]
+    rd = buf[384:384 + min(nb, 256)].astype(np.int64) - t0
+    print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} "
+          f"fb={out.fallback_used} scanner CTA {int(buf[31])}")
+    print(f"   rows done per CTA: first {rd.min() / 1e3:.2f} median {np.median(rd) / 1e3:.2f} "
+          f"last {rd.max() / 1e3:.2f} us")
+    for slot in sorted(names, key=lambda s: int(buf[s]) if buf[s] else 1 << 62):
+        if buf[slot]:
+            print(f"   {names[slot]:>22s}: {(int(buf[slot]) - t0) / 1000:8.2f} us")
+    if i > 6:
+        break
