@@ -65,7 +65,8 @@ def parse():
     ap.add_argument("--first-wave-tokens", type=int, default=0)
     ap.add_argument("--direct", action="store_true", help="launch kernels without the CUDA graph (profiling)")
     ap.add_argument("--no-batch", action="store_true", help="skip the batched (c3) measurement")
-    ap.add_argument("--batch-steps", type=int, default=40)
+    ap.add_argument("--batch-steps", type=int, default=20)
+    ap.add_argument("--no-big", action="store_true", help="skip the c4 / c5 batched measurements")
     ap.add_argument("--sharded-steps", type=int, default=20)
     return ap.parse_args()
 
@@ -196,72 +197,144 @@ def cpu_baseline(T, ix, q, cfg, seconds, ours=None):
             "fallback_rate": fb / max(n, 1), "parity_vs_gpu": parity}
 
 
-C3 = dict(V=151552, d=3584, C=2273, g=1, dtype="bf16", B=16, eps=1e-3)
+C3 = dict(name="qwen2.5-head", V=151552, d=3584, C=2273, g=1, dtype="bf16", Bs=(16,), eps=1e-3,
+          targets=("softmax_eps",))
+# configs[3] / configs[4] on one B200 (their multi-GPU sharding is the
+# `sharded` object at N > 1): Llama-3 70B head at B=64, Gemma2 head B sweep
+C4 = dict(name="llama3-70b-head", V=128256, d=8192, C=1024, g=16, dtype="f32", Bs=(64,), eps=0.05,
+          targets=("topk", "softmax_eps"))
+C5 = dict(name="gemma2-head", V=256000, d=3584, C=3840, g=16, dtype="bf16", Bs=(1, 16, 64, 128), eps=0.05,
+          targets=("topk", "softmax_eps"))
 
 
-def run_batched(a, torch, P, lib, ctypes):
-    """configs[2] (c3): Qwen2.5 head V=151552 d=3584 bf16, C=2273, batch 16,
-    epsilon-certified softmax eps=1e-3.  One graph replay decodes the whole
-    batch (B concurrent step lanes + shared batched bounds)."""
+def run_batched(a, torch, P, lib, ctypes, c=C3, dense=False):
+    """A batched configuration: one graph replay decodes the whole batch
+    (shared batched bounds + B concurrent step lanes).  Device-timed replays
+    with L2 flushed before each, plus e2e through decode_step_batch (host
+    queries in, host outcomes out).  dense: also time the on-GPU dense
+    comparators for the same B (the exact f64 K5 GEMV once per query, and a
+    cuBLAS bf16 [V,d]x[d,B] GEMM as the library reference point)."""
     from paper_2511_21702_b200 import workload as wl
-    c = C3
+    t_setup = time.time()
     T = wl.synth_vocab(c["V"], c["d"], c["C"] // c["g"], a.spread, 1, dtype=c["dtype"])
     ix = wl.fast_index(T, c["C"] // c["g"], c["g"])
-    B, K = c["B"], a.batch_steps
-    Q = wl.generate_queries(B * (K + 3), c["d"], "contextual", 7, centroids=ix.centroids, noise=a.noise)
-    cfg = P.DecodeConfig(k=a.k, epsilon=c["eps"], targets=("softmax_eps",))
+    K = a.batch_steps
+    Bmax = max(c["Bs"])
+    Q = wl.generate_queries(Bmax * (K + 3), c["d"], "contextual", 7, centroids=ix.centroids, noise=a.noise)
+    cfg = P.DecodeConfig(k=a.k, epsilon=c["eps"], targets=c["targets"])
     ctx = P.prepare(T, ix)
     ccfg = ctx.make_config(cfg)
     sp = ctypes.c_void_p()
     lib.csvd_stream(ctx._ctx, ctypes.byref(sp))
     ext = torch.cuda.ExternalStream(sp.value)
     Hd = torch.from_numpy(Q).cuda()
-    # e2e through the public API: host queries in, host outcomes out
-    for i in range(3):
-        P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
-    e2e_t, outs = [], []
-    for i in range(3, K + 3):
-        lib.csvd_l2_flush(ctx._ctx, sp)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        o = P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
-        e2e_t.append(time.perf_counter() - t0)
-        outs += o
-    dev_ms = []
-    for i in range(K + 3):
-        lib.csvd_l2_flush(ctx._ctx, sp)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(ext)
-        rc = lib.csvd_step_batch_device(ctx._ctx, B, Hd[i * B:(i + 1) * B].data_ptr(), ctypes.byref(ccfg), sp)
-        e1.record(ext)
-        if rc != 0:
-            raise RuntimeError(lib.csvd_strerror(ctx._ctx).decode())
-        torch.cuda.synchronize()
-        if i >= 3:
-            dev_ms.append(e0.elapsed_time(e1))
-    ms = float(np.mean(dev_ms))
-    d, Cn = c["d"], ix.n_clusters
-    # algorithmic bytes per batch (SURVEY §8d, batched): centroids once, the
-    # B queries, the union of opened rows (bf16 + f32 bias), ids + logits out
-    union_rows = 0
-    for j in range(K):
-        grp = outs[j * B:(j + 1) * B]
-        union_rows += len(set().union(*[set(o.token_ids.tolist()) for o in grp]))
-    union_rows /= K
-    sub = float(np.mean([o.stats.sub_size for o in outs]))
-    bytes_b = 8 * Cn * d + 24 * Cn + B * 8 * d + union_rows * (2 * d + 4) + B * 12 * sub
+    d, Cn, V = c["d"], ix.n_clusters, c["V"]
+    s_w = 2 if c["dtype"] == "bf16" else 4
     pk, _ = peaks()
-    return {
-        "workload": f"qwen2.5-head V={c['V']} d={d} C={Cn} bf16 B={B} softmax_eps eps={c['eps']}",
-        "value": B * 1e3 / ms, "unit": "query-steps/s", "ms_per_batch": ms,
-        "e2e": {"value": B * K / sum(e2e_t), "unit": "query-steps/s",
-                "h2d_bytes_per_step": B * 8 * d + 152, "d2h_bytes_per_step": float(B * 88 + 16 * B * sub)},
-        "roofline": {"bound": "hbm", "achieved": bytes_b / (ms * 1e-3) / 1e9, "peak": pk, "unit": "GB/s",
-                     "frac": bytes_b / (ms * 1e-3) / 1e9 / pk, "algorithmic_bytes_per_batch": bytes_b},
-        "mean_sub_size": sub, "mean_clusters_opened": float(np.mean([o.stats.clusters_opened for o in outs])),
-        "fallback_rate": float(np.mean([o.fallback_used is not None for o in outs])),
-        "design": "B concurrent step lanes (cooperative grids of 148/B CTAs) after one shared batched-bounds kernel",
-    }
+    setup_s = time.time() - t_setup
+    res = []
+    for B in c["Bs"]:
+        # e2e through the public API: host queries in, host outcomes out
+        for i in range(3):
+            P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
+        e2e_t, outs = [], []
+        for i in range(3, K + 3):
+            lib.csvd_l2_flush(ctx._ctx, sp)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            o = P.decode_step_batch(T, ix, Q[i * B:(i + 1) * B], cfg)
+            e2e_t.append(time.perf_counter() - t0)
+            outs += o
+        dev_ms = []
+        for i in range(K + 3):
+            lib.csvd_l2_flush(ctx._ctx, sp)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            rc = lib.csvd_step_batch_device(ctx._ctx, B, Hd[i * B:(i + 1) * B].data_ptr(), ctypes.byref(ccfg), sp)
+            e1.record(ext)
+            if rc != 0:
+                raise RuntimeError(lib.csvd_strerror(ctx._ctx).decode())
+            torch.cuda.synchronize()
+            if i >= 3:
+                dev_ms.append(e0.elapsed_time(e1))
+        ms = float(np.mean(dev_ms))
+        # algorithmic bytes per batch (SURVEY §8d, batched): centroids once, the
+        # B queries, the union of opened rows (+ bias), ids + logits out; a
+        # full-vocabulary fallback query adds the whole table
+        union_rows = 0
+        for j in range(K):
+            grp = outs[j * B:(j + 1) * B]
+            if any(o.fallback_used == "full_vocab" for o in grp):
+                union_rows += V
+            else:
+                union_rows += len(set().union(*[set(o.token_ids.tolist()) for o in grp]))
+        union_rows /= K
+        sub = float(np.mean([o.stats.sub_size for o in outs]))
+        bytes_b = 8 * Cn * d + 24 * Cn + B * 8 * d + union_rows * (s_w * d + 4) + B * 12 * sub
+        r = {
+            "B": B, "value": B * 1e3 / ms, "unit": "query-steps/s", "ms_per_batch": ms,
+            "e2e": {"value": B * K / sum(e2e_t), "unit": "query-steps/s",
+                    "h2d_bytes_per_step": B * 8 * d + 152, "d2h_bytes_per_step": float(B * 88 + 16 * B * sub)},
+            "roofline": {"bound": "hbm", "achieved": bytes_b / (ms * 1e-3) / 1e9, "peak": pk, "unit": "GB/s",
+                         "frac": bytes_b / (ms * 1e-3) / 1e9 / pk, "algorithmic_bytes_per_batch": bytes_b},
+            "mean_sub_size": sub, "mean_clusters_opened": float(np.mean([o.stats.clusters_opened for o in outs])),
+            "fallback_rate": float(np.mean([o.fallback_used is not None for o in outs])),
+        }
+        if dense:
+            dm = []
+            for i in range(4):
+                lib.csvd_l2_flush(ctx._ctx, sp)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(ext)
+                for b in range(B):
+                    lib.csvd_dense_device(ctx._ctx, Hd[b].data_ptr(), sp)
+                e1.record(ext)
+                torch.cuda.synchronize()
+                if i >= 1:
+                    dm.append(e0.elapsed_time(e1))
+            dms = float(np.mean(dm))
+            r["dense_exact_f64_gemv"] = {"ms_per_batch": dms, "query_steps_per_s": B * 1e3 / dms,
+                                         "sparse_speedup": dms / ms}
+            r["dense_cublas_bf16_gemm"] = cublas_dense(torch, V, d, B, Hd[:B])
+            r["dense_cublas_bf16_gemm"]["sparse_speedup"] = r["dense_cublas_bf16_gemm"]["ms_per_batch"] / ms
+        res.append(r)
+    del ctx
+    engine_clear()
+    out = {"workload": f"{c['name']} V={V} d={d} C={Cn} g={c['g']} {c['dtype']} "
+                       f"targets={'+'.join(c['targets'])} eps={c['eps']} k={a.k}",
+           "setup_s": setup_s,
+           "design": "shared batched bounds + B concurrent step lanes (cooperative grid of 148/B CTAs each)"}
+    if len(res) == 1:
+        out.update(res[0])
+    else:
+        out["sweep"] = res
+    return out
+
+
+def engine_clear():
+    from paper_2511_21702_b200 import engine
+    engine.clear_cache()
+
+
+def cublas_dense(torch, V, d, B, Hd):
+    """Library reference point for the dense comparator: torch.matmul (cuBLAS)
+    of a random bf16 [V, d] table with the B queries in bf16, fp32 out."""
+    W = torch.randn(V, d, device="cuda", dtype=torch.bfloat16)
+    Hb = Hd.to(torch.bfloat16).t().contiguous()
+    flush = torch.empty(96 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    ts = []
+    for i in range(6):
+        flush.add_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(W, Hb)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(e0.elapsed_time(e1))
+    del W, flush
+    ms = float(np.mean(ts))
+    return {"ms_per_batch": ms, "query_steps_per_s": B * 1e3 / ms, "note": "not exact: bf16 in / bf16 out, fp32 accumulate"}
 
 
 def run_sharded(a, torch, P, dist, world, rank, T, ix, q):
@@ -426,7 +499,12 @@ def run_ours(a):
         if world > 1:
             dist.destroy_process_group()
         return
-    batched = None if (a.no_batch or world > 1) else run_batched(a, torch, P, lib, ctypes)
+    batched = {}
+    if not (a.no_batch or world > 1):
+        batched["batched_c3"] = run_batched(a, torch, P, lib, ctypes, C3)
+        if not a.no_big:
+            batched["batched_c4"] = run_batched(a, torch, P, lib, ctypes, C4)
+            batched["batched_c5_sweep"] = run_batched(a, torch, P, lib, ctypes, C5, dense=True)
     pk, pk_kind = peaks()
     bytes_steps = [step_bytes(ix, o, s_w) for o in outs]
     mean_bytes = float(np.mean(bytes_steps))
@@ -484,8 +562,7 @@ def run_ours(a):
         "gpu_launches": K * (1 if a.no_flush else 2),
         "clocks": clk.summary(),
     }
-    if batched is not None:
-        line["batched_c3"] = batched
+    line.update(batched)
     if sharded is not None:
         line["sharded"] = sharded
     if not a.no_cpu_baseline:

@@ -23,11 +23,14 @@ __global__ void k_permute_rows(const char *src, char *dst, const long long *perm
     for (long long pos = blockIdx.x; pos < V; pos += gridDim.x) {
         const char *s = src + perm[pos] * row_bytes;
         char *t = dst + pos * row_bytes;
-        for (long long b = threadIdx.x * 16; b < row_bytes; b += blockDim.x * 16) {
-            if (b + 16 <= row_bytes)
+        if ((row_bytes & 15) == 0) {  // 16-byte rows: vector copies
+            for (long long b = threadIdx.x * 16; b < row_bytes; b += blockDim.x * 16)
                 *reinterpret_cast<uint4 *>(t + b) = *reinterpret_cast<const uint4 *>(s + b);
-            else
-                for (long long j = b; j < row_bytes; ++j) t[j] = s[j];
+        } else if ((row_bytes & 3) == 0) {  // odd d: rows are only 4-byte aligned
+            for (long long b = threadIdx.x * 4; b < row_bytes; b += blockDim.x * 4)
+                *reinterpret_cast<unsigned *>(t + b) = *reinterpret_cast<const unsigned *>(s + b);
+        } else {
+            for (long long b = threadIdx.x; b < row_bytes; b += blockDim.x) t[b] = s[b];
         }
     }
 }
@@ -483,6 +486,12 @@ static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
         cudaGraphDestroy(g);
         return fail(ctx, CSVD_ECUDA, std::string("head graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
     }
+    if (getenv("CSVD_HEAD_NOCOND")) {  // measurement only: the head kernel alone (undecided steps are wrong)
+        e = cudaGraphInstantiate(out, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("head graph: ") + cudaGetErrorString(e));
+        return 0;
+    }
     // the leaf (k_head) node
     size_t n = 0;
     CK(cudaGraphGetNodes(g, nullptr, &n));
@@ -593,8 +602,6 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     if ((int)ctx->lanes.size() == B && ctx->lane_grid == G && ctx->lane_K == D0.K) return 0;
     free_lanes(ctx);
     const int C = D0.C, V = D0.V, K = D0.K;
-    if ((long long)C > (long long)MAX_PER_WARP * G * WARPS)
-        return fail(ctx, CSVD_ECONFIG, "too many clusters for a batch lane's grid (use a smaller batch)");
     int rc;
     if ((rc = lalloc(ctx, &ctx->d_H, (size_t)B * D0.d))) return rc;
     if ((rc = lalloc(ctx, &ctx->d_res_all, (size_t)B))) return rc;

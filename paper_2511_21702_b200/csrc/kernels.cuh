@@ -367,17 +367,22 @@ __device__ void bounds_phase(const Dev &D, const double *hs, double *scratch) {
         }
         if (lane == 0) s_qn = __dsqrt_rn(ss);
     }
+    // a warp's first MAX_PER_WARP dots wait in shared memory for ||h||; any
+    // further ones (small lane grids, large C) wait in D.dots (same thread)
     int j = 0;
-    for (int c = warp * CTA_N + CTA_ID; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
+    for (int c = warp * CTA_N + CTA_ID; c < D.C; c += stride, ++j) {
         double dot = warp_dot_t<double, BCPL, BQ>(D.cent + (size_t)c * D.bd, hs, D.bplan, scratch, lane);
-        if (lane == 0) s_dot[warp][j] = dot;
+        if (lane == 0) {
+            if (j < MAX_PER_WARP) s_dot[warp][j] = dot;
+            else D.dots[c] = dot;
+        }
     }
     __syncthreads();
     const double qn = s_qn;
     if (lane == 0) {
         j = 0;
-        for (int c = warp * CTA_N + CTA_ID; c < D.C && j < MAX_PER_WARP; c += stride, ++j) {
-            const double dot = s_dot[warp][j];
+        for (int c = warp * CTA_N + CTA_ID; c < D.C; c += stride, ++j) {
+            const double dot = j < MAX_PER_WARP ? s_dot[warp][j] : D.dots[c];
             double u;
             if (D.mode == CSVD_MODE_SPHERICAL)
                 u = cone_bound(D, c, dot, qn);

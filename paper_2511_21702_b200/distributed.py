@@ -286,6 +286,18 @@ class ShardedDecoder:
         self.backend = backend
         self.V, self.C, self.d = int(index.vocab_size), int(index.n_clusters), int(index.hidden_dim)
 
+    def check_same_inputs(self, h, cfg, k_max):
+        """Every rank must decode the same query with the same config (the
+        workers of one sharded step): all_gather a digest and compare."""
+        import hashlib
+        m = hashlib.sha256(np.ascontiguousarray(h, dtype=np.float64).tobytes())
+        m.update(repr((cfg.k, cfg.epsilon, tuple(cfg.targets), cfg.k_max, tuple(map(repr, cfg.fallback)),
+                       getattr(cfg, "slack_mode", "none"), k_max)).encode())
+        dig = np.frombuffer(m.digest()[:16], dtype=np.int64)
+        got = self.comm.all_gather(dig)
+        if any(not np.array_equal(g, dig) for g in got):
+            raise ValueError("sharded step: ranks passed different queries or configs")
+
     def _open(self, st: MergedState, h, cs, lo, hi, parts):
         summ, pos, ids, logits = self.backend.open(h, cs, lo, hi)
         sums = self.comm.all_gather(summ)

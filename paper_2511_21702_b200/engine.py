@@ -142,6 +142,17 @@ class DeviceIndex:
             self._ctx = None
             _raise(rc, msg)
         self._lib = lib
+        # The upload is keyed on object identity (the reference re-hashes the
+        # table every step, decode.py:324): freeze the uploaded host arrays so
+        # an in-place change raises instead of silently diverging from the
+        # device copy.
+        for a in (getattr(table, "weights", None), getattr(table, "bias", None), index.centroids, index.radii,
+                  index.max_biases, index.perm, index.starts, index.sizes):
+            if isinstance(a, np.ndarray) and a.flags.writeable:
+                try:
+                    a.flags.writeable = False
+                except ValueError:
+                    pass
         self._cfg_cache = {}
         self._lock = threading.Lock()
         self._res = _lib.Result()
@@ -310,8 +321,17 @@ def config_struct(cfg, V: int, k_max=None, variant=_lib.VARIANT_INCREMENTAL,
 # context cache: one upload per (table, index) pair
 # ---------------------------------------------------------------------------
 _CACHE: dict = {}
-_CACHE_LOCK = threading.Lock()
+_CACHE_LOCK = threading.RLock()  # re-entrant: eviction callbacks may fire inside a locked section
 DEFAULT_DEVICE = 0
+
+
+def _evict(key, ref):
+    """weakref callback: a cached table / index died -> free its device context."""
+    with _CACHE_LOCK:
+        ent = _CACHE.get(key)
+        if ent is not None and any(r is ref for r in ent[0]):
+            del _CACHE[key]
+            ent[1].close()
 
 
 def _cache_get(key, objs, factory):
@@ -321,8 +341,10 @@ def _cache_get(key, objs, factory):
             refs, ctx = ent
             if all(r() is o for r, o in zip(refs, objs)):
                 return ctx
+            del _CACHE[key]
+            ctx.close()
         ctx = factory()
-        refs = tuple(weakref.ref(o) for o in objs)
+        refs = tuple(weakref.ref(o, lambda r, k=key: _evict(k, r)) for o in objs)
         _CACHE[key] = (refs, ctx)
         return ctx
 

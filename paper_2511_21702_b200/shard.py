@@ -21,6 +21,7 @@ the worker count visible only in the `CommLedger` byte accounting.
 from __future__ import annotations
 
 import json
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -232,36 +233,39 @@ def ledger_for(index, plan: ShardPlan, outcome, latency: LatencyModel = LatencyM
 _DECODERS: dict = {}
 
 
-def _distributed_world():
-    try:
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized():
-            return dist.get_world_size()
-    except Exception:  # pragma: no cover
-        pass
-    return 1
-
-
-def sharded_decode_step(table, index, plan: ShardPlan, h, cfg, k_max=None, latency: LatencyModel = LatencyModel()):
+def sharded_decode_step(table, index, plan: ShardPlan, h, cfg, k_max=None, latency: LatencyModel = LatencyModel(),
+                        group=None):
     """B200 `csvd.sharded_decode_step` (shard_sim.py:134-208).
 
-    Inside a torch.distributed process group whose size equals
-    plan.n_workers, every rank is one worker: it owns the plan's clusters on
-    its GPU and the step runs as `distributed.ShardedDecoder` (one all_gather
-    of per-shard merge records).  Otherwise (one process) the N workers are
-    simulated as in the reference: the outcome is the batch-select step,
-    bit-identical for every N and strategy by construction.  Either way the
-    ledger is the reference's accounting."""
+    group=None (the reference's call): the N workers are simulated as in the
+    reference, and the outcome is the batch-select step, bit-identical for
+    every N and strategy by construction.  group=<torch.distributed process
+    group of plan.n_workers ranks> (opt-in): every rank is one worker, owns
+    the plan's clusters on its GPU, and the step runs as
+    `distributed.ShardedDecoder` (one all_gather of per-shard merge records);
+    every rank must pass the same h / cfg, which is cross-checked by digest.
+    Either way the ledger is the reference's accounting."""
     validate_config(cfg, index.vocab_size)
     if np.asarray(plan.assignment).shape != (index.n_clusters,):
         raise ValueError("plan does not cover this index")
     k_max = resolved_k_max(cfg, index.vocab_size) if k_max is None else k_max
-    if plan.n_workers > 1 and _distributed_world() == plan.n_workers:
-        from .distributed import ShardedDecoder
-        key = (id(table), id(index), id(plan))
-        dec = _DECODERS.get(key)
+    if group is not None and plan.n_workers > 1:
+        import torch.distributed as dist
+        from .distributed import ShardedDecoder, TorchComm
+        if dist.get_world_size(group) != plan.n_workers:
+            raise ValueError(f"process group has {dist.get_world_size(group)} ranks, plan has {plan.n_workers}")
+        key = (id(table), id(index), id(plan), id(group))
+        ent = _DECODERS.get(key)
+        dec = None
+        if ent is not None:
+            refs, dec = ent
+            if not all(r() is o for r, o in zip(refs, (table, index, plan))):
+                dec = None
         if dec is None:
-            dec = _DECODERS[key] = ShardedDecoder(table, index, plan)
+            dec = ShardedDecoder(table, index, plan, comm=TorchComm(group))
+            refs = tuple(weakref.ref(o, lambda _r, k=key: _DECODERS.pop(k, None)) for o in (table, index, plan))
+            _DECODERS[key] = (refs, dec)
+        dec.check_same_inputs(h, cfg, k_max)
         outcome = dec.step(h, cfg, k_max=k_max)
     else:
         outcome = engine.decode_step_batchselect(table, index, h, cfg, k_max=k_max)
