@@ -471,8 +471,8 @@ static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
     cudaStream_t s = ctx->stream;
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphConditionalHandle h = 0;
+    if (!getenv("CSVD_HEAD_NOCOND")) CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
     CK(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
     Dev D = host_io ? ctx->Dhost : ctx->D;

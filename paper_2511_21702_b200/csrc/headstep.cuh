@@ -173,13 +173,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
             D.ids_host[r] = __ldcg(D.S_ids + r);
         }
     }
+    if (D.dbg && tid == 0 && b < 256) D.dbg[128 + b] = gtimer();  // per-CTA: summaries done
     if (!s_last) return;
     // ---- the last CTA: certification scan over the head (scan.cuh)
     __threadfence();
     if (D.dbg && tid == 0) {
         DBG_TS(D, 29);
         D.dbg[31] = (unsigned long long)b;
+        g_dbg_cta = b;
     }
+    __syncthreads();
     double *c_vals = sws, *c_lse = sws + 6 * CHUNK, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
     double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
     double reg_list = -INFINITY;
@@ -211,8 +214,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
             s2.iter = 1;
             *D.st = s2;
             if (D.res_host) *D.res_host = r;
-            cudaGraphSetConditional(cond, 0);  // decided: skip the general step
+            if (cond) cudaGraphSetConditional(cond, 0);  // decided: skip the general step
         }
         DBG_TS(D, 30);
+        if (D.dbg) g_dbg_cta = 0;
     }
 }

@@ -129,6 +129,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// the CTA whose phases the debug timestamps of shared helpers follow (CTA 0
+// in k_step; the scanning CTA in k_head)
+static __device__ int g_dbg_cta = 0;
+#define DBG_HERE(D) ((D).dbg && (int)blockIdx.x == g_dbg_cta)
 #define DBG_TS(D, slot)                                    \
     do {                                                   \
         if ((D).dbg) {                                     \
@@ -879,10 +883,10 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
             mn = fmin(mn, x);
         }
     }
-    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 48);
+    if (DBG_HERE(D) && threadIdx.x == 0) DBG_TS(D, 48);
     mx = warp_max(mx);
     mn = warp_min(mn);
-    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 49);
+    if (DBG_HERE(D) && threadIdx.x == 0) DBG_TS(D, 49);
     double s = 0.0;
     if (in_regs) {
 #pragma unroll
@@ -892,7 +896,7 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
         for (int i = lane; i < n; i += 32) s = __dadd_rn(s, csvd_exp(__dsub_rn(__ldcg(v + i), mx)));
     }
     s = warp_sum(s);
-    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 50);
+    if (DBG_HERE(D) && threadIdx.x == 0) DBG_TS(D, 50);
     if (in_regs) {
         // top-kk values (only the values matter: the list holds no ids).
         // Each lane sorts its 8 values (Batcher network), then kk rounds of a
@@ -912,7 +916,7 @@ static __device__ __forceinline__ void cluster_summary(const Dev &D, int lo, int
         CSVD_CAS(2, 4) CSVD_CAS(3, 5)
         CSVD_CAS(3, 4)
 #undef CSVD_CAS
-    if (D.dbg && CTA_ID == 0 && threadIdx.x == 0) DBG_TS(D, 51);
+    if (DBG_HERE(D) && threadIdx.x == 0) DBG_TS(D, 51);
 #pragma unroll 1
         for (int j = 0; j < kk; ++j) {
             const unsigned long long key = dkey(reg[0]);
@@ -1057,7 +1061,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
         pmn = fmin(pmn, st0.smin);
         pmx = fmax(pmx, st0.smax);
     }
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 40);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 40);
     // streaming log Z_S (certify.py:83 logaddexp chain) as a prefix sum of
     // exp(lse - M) over the chunk, M the chunk's largest term (incl. the carry)
     double lz;
@@ -1076,7 +1080,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             lz = t > 0.0 ? __dadd_rn(M, csvd_log(t)) : -INFINITY;
         }
     }
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 41);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 41);
     // the reference recomputes log Z_S over all of S when the merge count p % 64 == 0
     const int rlane = (q0 / 64) * 64 + 63 - q0;
     if (rlane < q1 - q0) {
@@ -1099,7 +1103,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
         if (lane == rlane) lz = full;
         if (lane > rlane) lz = (mm == -INFINITY) ? -INFINITY : __dadd_rn(mm, csvd_log(sv));
     }
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 42);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 42);
     // k-th largest after each merge (exact)
     double my_kth = -INFINITY;
     int kc = ss.kcount;
@@ -1148,7 +1152,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             __syncwarp();
         }
     }
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 43);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 43);
     double *c_lz = c_vals, *c_kth = c_vals + CHUNK, *c_mn = c_vals + 2 * CHUNK, *c_mx = c_vals + 3 * CHUNK;
     double *c_rho = c_vals + 4 * CHUNK, *c_dl = c_vals + 5 * CHUNK;
     if (act) {
@@ -1166,7 +1170,7 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
     ScanState stl = st0;
     Scan sc{in, stl, res};
     const csvd_config &cfg = *D.cfg;
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 44);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 44);
     if (stl.phase == PH_MAIN && cfg.variant == CSVD_VARIANT_INCREMENTAL) {
         // Common path, all prefixes of the chunk at once: the first prefix that
         // trips the budget (decode.py:342) or passes a target (decode.py:192-210).
@@ -1194,9 +1198,9 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
             stl.heap_pops = stl.p;
         }
     }
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 45);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 45);
     sc.run(chk);
-    if (CTA_ID == 0 && lane == 0) DBG_TS(D, 46);
+    if (DBG_HERE(D) && lane == 0) DBG_TS(D, 46);
     __syncwarp();
     if (lane == 0) {
         ss.st = stl;

@@ -164,10 +164,80 @@ __host__ __device__ inline int pw_hs_size(const PwPlan &pl) {
     return (pl.regular && pl.cpl == 8) ? pl.n + 2 * pl.nleaf : pl.n;
 }
 
+// CPL = 8 (one leaf per lane): the leaf's loads double-buffered, so the next
+// batch is in flight while the current one is multiplied and summed (the
+// row's load latency overlaps the f64 work instead of alternating with it)
+template <typename ET, int Q>
+__device__ __forceinline__ double warp_dot_r8(const ET *__restrict__ row, const double *__restrict__ hs,
+                                              int leaf_len, int lane) {
+    constexpr int NB = NBatch<ET, 8>::value / 2;  // loads per buffer
+    const int S = leaf_len >> 3;
+    double slice[Q];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+        const ET *lp = row + (size_t)(u * 32 + lane) * leaf_len;
+        const double *hp = hs + (size_t)(u * 32 + lane) * (leaf_len + 2);
+        double r[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) r[c] = 0.0;
+        Raw<ET, 8> A[NB], B[NB];
+#pragma unroll
+        for (int s = 0; s < NB; ++s)
+            if (s < S) A[s].load(lp + s * 8);
+        auto consume = [&](const Raw<ET, 8>(&buf)[NB], int i0) {
+#pragma unroll
+            for (int s = 0; s < NB; ++s) {
+                const int i = i0 + s;
+                if (i < S) {
+                    const double2 *h2 = reinterpret_cast<const double2 *>(hp + 8 * i);
+                    double hv[8];
+#pragma unroll
+                    for (int c2 = 0; c2 < 4; ++c2) {
+                        const double2 t = h2[c2];
+                        hv[2 * c2] = t.x;
+                        hv[2 * c2 + 1] = t.y;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double p = d_mul(buf[s].get(c), hv[c]);
+                        r[c] = (i == 0) ? p : d_add(r[c], p);
+                    }
+                }
+            }
+        };
+#pragma unroll 1
+        for (int i0 = 0; i0 < S; i0 += 2 * NB) {
+#pragma unroll
+            for (int s = 0; s < NB; ++s)
+                if (i0 + NB + s < S) B[s].load(lp + (i0 + NB + s) * 8);
+            consume(A, i0);
+#pragma unroll
+            for (int s = 0; s < NB; ++s)
+                if (i0 + 2 * NB + s < S) A[s].load(lp + (i0 + 2 * NB + s) * 8);
+            consume(B, i0 + NB);
+        }
+        double v = d_add(d_add(d_add(r[0], r[1]), d_add(r[2], r[3])), d_add(d_add(r[4], r[5]), d_add(r[6], r[7])));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
+        slice[u] = v;
+    }
+    double tot;
+    if constexpr (Q == 1)
+        tot = slice[0];
+    else if constexpr (Q == 2)
+        tot = d_add(slice[0], slice[1]);
+    else
+        tot = d_add(d_add(slice[0], slice[1]), d_add(slice[2], slice[3]));
+    return d_add(0.0, tot);
+}
+
 template <typename ET, int CPL, int Q>
 __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
                                                    const double *__restrict__ hs,
                                                    int leaf_len, int lane) {
+#ifndef CSVD_NO_PIPE
+    if constexpr (CPL == 8) return warp_dot_r8<ET, Q>(row, hs, leaf_len, lane);
+#endif
     constexpr int LPL = 8 / CPL;   // lanes per leaf
     constexpr int NLW = 32 / LPL;  // leaves per slice
     constexpr int NB = NBatch<ET, CPL>::value;
