@@ -90,7 +90,7 @@ struct csvd_ctx {
     double *logits_pin = nullptr;
     cudaGraphExec_t g_step = nullptr, g_host = nullptr, g_bounds = nullptr, g_dense = nullptr;
     // head step (headstep.cuh): [h2d] -> k_head -> IF(undecided) k_step
-    void (*khead)(Dev, cudaGraphConditionalHandle) = nullptr;
+    void (*khead)(Dev) = nullptr;
     cudaGraphExec_t g_step_head = nullptr, g_host_head = nullptr;
     // zero-copy host results (csvd_step_host): mapped pinned buffers + flag
     csvd_result *res_map = nullptr;
@@ -219,12 +219,12 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
 CSVD_EXTERN_ET(float)
 CSVD_EXTERN_ET(uint16_t)
 #define CSVD_EXTERN_HEAD(ET) \
-    extern template __global__ void k_head<ET, 1>(const __grid_constant__ Dev, cudaGraphConditionalHandle); \
-    extern template __global__ void k_head<ET, 2>(const __grid_constant__ Dev, cudaGraphConditionalHandle); \
-    extern template __global__ void k_head<ET, 4>(const __grid_constant__ Dev, cudaGraphConditionalHandle);
+    extern template __global__ void k_head<ET, 1>(const __grid_constant__ Dev); \
+    extern template __global__ void k_head<ET, 2>(const __grid_constant__ Dev); \
+    extern template __global__ void k_head<ET, 4>(const __grid_constant__ Dev);
 CSVD_EXTERN_HEAD(float)
 CSVD_EXTERN_HEAD(uint16_t)
-typedef void (*khead_t)(Dev, cudaGraphConditionalHandle);
+typedef void (*khead_t)(Dev);
 template <typename ET>
 static khead_t pick_head_t(const PwPlan &wp) {
     switch (wp.q) {
@@ -465,58 +465,22 @@ static int capture(csvd_ctx *ctx, int mode, bool host_io, cudaGraphExec_t *out) 
     return 0;
 }
 
-// [h2d h] -> k_head -> IF(handle) { k_step }: the handle defaults to 1 every
-// replay; k_head sets it to 0 once it has decided the step.
+// [h2d h] -> k_head (which runs the general step itself when the head cannot
+// decide): one kernel node per step
 static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
     cudaStream_t s = ctx->stream;
     cudaGraph_t g;
-    CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h = 0;
-    if (!getenv("CSVD_HEAD_NOCOND")) CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-    CK(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
     Dev D = host_io ? ctx->Dhost : ctx->D;
     D.launch_mode = LAUNCH_STEP;
-    void *args[] = {&D, &h};
+    void *args[] = {&D};
     cudaError_t e = cudaLaunchCooperativeKernel((const void *)ctx->khead, dim3(ctx->grid), dim3(THREADS), args,
                                                 ctx->smem, s);
-    cudaGraph_t g2;
-    cudaError_t e2 = cudaStreamEndCapture(s, &g2);
+    cudaError_t e2 = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess || e2 != cudaSuccess) {
-        cudaGraphDestroy(g);
+        if (e2 == cudaSuccess) cudaGraphDestroy(g);
         return fail(ctx, CSVD_ECUDA, std::string("head graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
-    }
-    if (getenv("CSVD_HEAD_NOCOND")) {  // measurement only: the head kernel alone (undecided steps are wrong)
-        e = cudaGraphInstantiate(out, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("head graph: ") + cudaGetErrorString(e));
-        return 0;
-    }
-    // the leaf (k_head) node
-    size_t n = 0;
-    CK(cudaGraphGetNodes(g, nullptr, &n));
-    std::vector<cudaGraphNode_t> nodes(n);
-    CK(cudaGraphGetNodes(g, nodes.data(), &n));
-    cudaGraphNode_t leaf = nullptr;
-    for (cudaGraphNode_t nd : nodes) {
-        size_t nd_out = 0;
-        CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out));
-        if (nd_out == 0) leaf = nd;
-    }
-    cudaGraphNodeParams p = {};
-    p.type = cudaGraphNodeTypeConditional;
-    p.conditional.handle = h;
-    p.conditional.type = cudaGraphCondTypeIf;
-    p.conditional.size = 1;
-    cudaGraphNode_t cn;
-    CK(cudaGraphAddNode(&cn, g, &leaf, 1, &p));
-    cudaGraph_t body = p.conditional.phGraph_out[0];
-    CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    int rc = launch(ctx, LAUNCH_STEP, s, host_io);
-    e2 = cudaStreamEndCapture(s, &g2);
-    if (rc || e2 != cudaSuccess) {
-        cudaGraphDestroy(g);
-        return rc ? rc : fail(ctx, CSVD_ECUDA, std::string("head graph body: ") + cudaGetErrorString(e2));
     }
     e = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);

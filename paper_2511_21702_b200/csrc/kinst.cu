@@ -12,5 +12,5 @@ template __global__ void k_dense_gemv<KI_ET, KI_CPL, KI_Q>(const __grid_constant
 template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q, true>(const __grid_constant__ Dev);  // grouped batch lanes
 #endif
 #if KI_CPL == 8
-template __global__ void k_head<KI_ET, KI_Q>(const __grid_constant__ Dev, cudaGraphConditionalHandle);  // the head step
+template __global__ void k_head<KI_ET, KI_Q>(const __grid_constant__ Dev);  // the head step
 #endif

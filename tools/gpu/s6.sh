@@ -1,0 +1,4 @@
+set -x
+timeout 300 python tools/head_times.py > gpurun_out/s6_head_times.txt 2>&1
+timeout 600 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --no-batch > gpurun_out/s6_bench.json 2> gpurun_out/s6_bench.err
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > gpurun_out/s6_pytest.txt

@@ -20,7 +20,7 @@ lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
 names = {24: "kernel start", 25: "h staged", 26: "cta0 bounds done", 27: "barrier passed", 28: "head done (cta0)",
-         29: "scanner start", 30: "scan done", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
+         29: "cta0: head rows complete", 31: "cta0: certified", 30: "decision published", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
          42: "scan: 64-merge recompute", 43: "scan: k-th merges", 44: "scan: rho/delta", 45: "scan: ballot+merge",
          46: "scan: state machine", 48: "summary: min/max", 49: "summary: warp min/max", 50: "summary: lse",
          51: "summary: sort"}
@@ -36,11 +36,11 @@ for i, h in enumerate(q):
     nb = ctx.info()["grid_ctas"]
     rd = buf[384:384 + min(nb, 256)].astype(np.int64) - t0
     print(f"step {i}: clusters={out.stats.clusters_opened} waves={ctx._res.waves} kind={out.status.kind} "
-          f"fb={out.fallback_used} scanner CTA {int(buf[31])}")
+          f"fb={out.fallback_used}")
     print(f"   rows done per CTA: first {rd.min() / 1e3:.2f} median {np.median(rd) / 1e3:.2f} "
           f"last {rd.max() / 1e3:.2f} us")
     sd = buf[128:128 + min(nb, 256)].astype(np.int64) - t0
-    print(f"   summaries done per CTA: first {sd.min() / 1e3:.2f} median {np.median(sd) / 1e3:.2f} "
+    print(f"   decision seen per CTA: first {sd.min() / 1e3:.2f} median {np.median(sd) / 1e3:.2f} "
           f"last {sd.max() / 1e3:.2f} us")
     for slot in sorted(names, key=lambda s: int(buf[s]) if buf[s] else 1 << 62):
         if buf[slot]:
