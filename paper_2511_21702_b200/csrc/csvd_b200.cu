@@ -122,12 +122,13 @@ struct csvd_ctx {
     cudaEvent_t fork = nullptr;
     double **d_Uraw_l = nullptr, **d_dots_l = nullptr;  // [lanes] per-lane bound outputs
     kern_t kgroup = nullptr;                      // grouped lanes kernel (one launch per batch)
+    kern_t kgroup_head = nullptr;                 // grouped head-step lanes (head-eligible configs)
     LaneWS *d_lanes = nullptr, *d_lanes_host = nullptr;
     void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *, int) = nullptr;
     size_t kbb_smem = 0;
     int kbb_gq = 0;
     cudaGraphExec_t g_batch = nullptr;
-    int g_batch_B = 0, g_batch_host = 0;
+    int g_batch_B = 0, g_batch_host = 0, g_batch_head = 0;
     csvd_result *res_map_b = nullptr;  // [lanes] mapped
     long long *ids_map_b = nullptr;    // [lanes, V] mapped
     double *logits_map_b = nullptr;    // [lanes, V] mapped
@@ -218,6 +219,12 @@ static int dupload(csvd_ctx *ctx, T **p, const T *src, size_t count) {
     CSVD_EXTERN_K(ET, 4, 1) CSVD_EXTERN_K(ET, 2, 1) CSVD_EXTERN_K(ET, 1, 1)
 CSVD_EXTERN_ET(float)
 CSVD_EXTERN_ET(uint16_t)
+#define CSVD_EXTERN_HEADL(ET) \
+    extern template __global__ void k_head_lanes<ET, 1>(const __grid_constant__ Dev); \
+    extern template __global__ void k_head_lanes<ET, 2>(const __grid_constant__ Dev); \
+    extern template __global__ void k_head_lanes<ET, 4>(const __grid_constant__ Dev);
+CSVD_EXTERN_HEADL(float)
+CSVD_EXTERN_HEADL(uint16_t)
 #define CSVD_EXTERN_HEAD(ET) \
     extern template __global__ void k_head<ET, 1>(const __grid_constant__ Dev); \
     extern template __global__ void k_head<ET, 2>(const __grid_constant__ Dev); \
@@ -240,6 +247,20 @@ static khead_t pick_head(const Dev &D) {
     if (!D.wplan.regular || D.wplan.cpl != 8 || D.wplan.n != D.bplan.n || D.mode == CSVD_MODE_BIAS_AUGMENTED)
         return nullptr;
     return D.wdtype == CSVD_W_BF16 ? pick_head_t<uint16_t>(D.wplan) : pick_head_t<float>(D.wplan);
+}
+template <typename ET>
+static kern_t pick_head_lanes_t(const PwPlan &wp) {
+    switch (wp.q) {
+        case 1: return k_head_lanes<ET, 1>;
+        case 2: return k_head_lanes<ET, 2>;
+        default: return k_head_lanes<ET, 4>;
+    }
+}
+static kern_t pick_head_lanes(const Dev &D) {
+    if (getenv("CSVD_NO_HEAD") || getenv("CSVD_NO_HEAD_LANES")) return nullptr;
+    if (!D.wplan.regular || D.wplan.cpl != 8 || D.wplan.n != D.bplan.n || D.mode == CSVD_MODE_BIAS_AUGMENTED)
+        return nullptr;
+    return D.wdtype == CSVD_W_BF16 ? pick_head_lanes_t<uint16_t>(D.wplan) : pick_head_lanes_t<float>(D.wplan);
 }
 // configs the head step can decide (everything else goes straight to k_step)
 static bool head_config(const csvd_config *cfg) {
@@ -597,6 +618,9 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             return rc;
         CK(cudaMemset(L.bar, 0, 16));
         CK(cudaMemset(L.st, 0, sizeof(ScanState)));
+        if ((rc = lalloc(ctx, &L.hcnt, (size_t)HMAX + 1)) || (rc = lalloc(ctx, &L.bar64, 4))) return rc;
+        CK(cudaMemset(L.hcnt, 0, sizeof(int) * (HMAX + 1)));
+        CK(cudaMemset(L.bar64, 0, 32));
         L.nblocks = G;
         L.dbg = nullptr;
         L.res_host = nullptr;
@@ -666,6 +690,8 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             w.res_host = L.res_host;
             w.ids_host = L.ids_host;
             w.logits_host = L.logits_host;
+            w.hcnt = L.hcnt;
+            w.bar64 = L.bar64;
             return w;
         };
         std::vector<LaneWS> td(B), th(B);
@@ -677,6 +703,14 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemcpy(ctx->d_lanes, td.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_lanes_host, th.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         ctx->kgroup = (getenv("CSVD_LANES_FORKED") || B * G > ctx->grid) ? nullptr : pick_grouped(D0);
+        ctx->kgroup_head = (ctx->kgroup && ctx->kbb) ? pick_head_lanes(D0) : nullptr;
+        if (ctx->kgroup_head) {
+            CK(cudaFuncSetAttribute((const void *)ctx->kgroup_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ctx->smem));
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kgroup_head, THREADS, ctx->smem));
+            if (occ * ctx->nsm < B * G) ctx->kgroup_head = nullptr;
+        }
         if (ctx->kgroup) {
             CK(cudaFuncSetAttribute((const void *)ctx->kgroup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->smem));
@@ -691,7 +725,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
 }
 
 // the batch graph: [H2D H, cfg] -> fork -> B lane kernels -> join [-> D2H results + first chunks]
-static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
+static int capture_batch(csvd_ctx *ctx, int B, bool host_io, bool head) {
     if (ctx->g_batch) cudaGraphExecDestroy(ctx->g_batch);
     ctx->g_batch = nullptr;
     cudaStream_t s = ctx->stream;
@@ -711,13 +745,15 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
         Dg.launch_mode = LAUNCH_STEP;
         Dg.lanes = host_io ? ctx->d_lanes_host : ctx->d_lanes;
         void *args[] = {&Dg};
-        CK(cudaLaunchCooperativeKernel((const void *)ctx->kgroup, dim3(B * ctx->lane_grid), dim3(THREADS), args,
+        const kern_t kl = (head && ctx->kgroup_head) ? ctx->kgroup_head : ctx->kgroup;
+        CK(cudaLaunchCooperativeKernel((const void *)kl, dim3(B * ctx->lane_grid), dim3(THREADS), args,
                                        ctx->smem, s));
         CK(cudaStreamEndCapture(s, &g));
         CK(cudaGraphInstantiate(&ctx->g_batch, g, 0));
         CK(cudaGraphDestroy(g));
         ctx->g_batch_B = B;
         ctx->g_batch_host = host_io ? 1 : 0;
+        ctx->g_batch_head = head ? 1 : 0;
         return 0;
     }
     CK(cudaEventRecord(ctx->fork, s));
@@ -737,6 +773,7 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io) {
     CK(cudaGraphDestroy(g));
     ctx->g_batch_B = B;
     ctx->g_batch_host = host_io ? 1 : 0;
+    ctx->g_batch_head = head ? 1 : 0;
     return 0;
 }
 
@@ -758,8 +795,10 @@ static int batch_prepare(csvd_ctx *ctx, int B, const csvd_config *cfg, bool host
     if (rc) return rc;
     if ((rc = ensure_lanes(ctx, B))) return rc;
     if ((rc = stage_pinned_cfg(ctx, ctx->cfg_pin_b, *cfg, s))) return rc;
-    if (!ctx->g_batch || ctx->g_batch_B != B || ctx->g_batch_host != (host_io ? 1 : 0))
-        if ((rc = capture_batch(ctx, B, host_io))) return rc;
+    const bool head = ctx->kgroup_head && head_config(cfg);
+    if (!ctx->g_batch || ctx->g_batch_B != B || ctx->g_batch_host != (host_io ? 1 : 0) ||
+        ctx->g_batch_head != (head ? 1 : 0))
+        if ((rc = capture_batch(ctx, B, host_io, head))) return rc;
     return 0;
 }
 

@@ -88,126 +88,101 @@ static __device__ __forceinline__ double head_bounds(const Dev &D, const double 
 // ---------------------------------------------------------------------------
 // Block-parallel certification of the head (CTA 0, all warps): every prefix
 // p = 1..hn of the head is tested at once instead of cluster by cluster.
-//   log Z_S(p)  = M + log(sum_{i < cum[p]} exp(S_i - M)): one block scan over
-//                 the positions (certify.py:79-83; the same value the
-//                 reference's logaddexp chain / 64-merge recompute converge
-//                 to, within ulps)
+//   log Z_S(p)  = M + log(sum over the first p clusters of exp(lse_q - M))
+//                 (certify.py:79-83; the value the reference's logaddexp chain
+//                 and its 64-merge recompute converge to, within ulps)
 //   top-k test  u_max(p) < kth(p)  <=>  #{i < cum[p] : S_i > Uo[p]} >= k
 //                 (certify.py:128-139): each logit adds 1 to every prefix from
 //                 max(q(i) + 1, first p with Uo[p] < S_i) on (Uo is
-//                 non-increasing), a histogram + prefix sum
+//                 non-increasing): a histogram + prefix sum
 //   rho / delta from log Z_S(p) and log R-hat(p)          (certify.py:93-107)
 // The first prefix with an event (budget overflow or a certified target, in
-// the configured target order; decode.py:192-210, 329-342) is the decision.
-// Its k-th logit (np.partition, certify.py:88), min / max (xi) follow by
-// block selections.  Returns 1 = decided (res filled), 0 = the step needs the
-// general path (overflow -> fallback chain, or no certificate in the head).
-// Logits live in registers: thread t holds positions [t*HJ, (t+1)*HJ).
-// ---------------------------------------------------------------------------
-#define HJ 16  // positions per thread: heads of up to THREADS * HJ = 4096 tokens
-static __device__ __forceinline__ bool head_fits(const Ord &o, int hn) { return o.cum[hn] <= THREADS * HJ; }
+// the configured target order; decode.py:192-210, 329-342) is the decision;
+// its k-th logit (np.partition, certify.py:88) comes from per-cluster top-k
+// lists, min / max (xi) from per-cluster extrema.  Returns 1 = decided (res
+// filled), 0 = the step needs the general path (overflow -> fallback chain,
+// or no certificate inside the head).
+static __device__ __forceinline__ bool head_fits(const Dev &D, const Ord &o, int hn) {
+    return hn * D.cfg->k <= pw_hs_size(D.wplan);  // the clusters' top-k lists fit where h was staged
+}
 
-static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int hn, csvd_result &res) {
+// Block-parallel certification.  Per cluster (warp w: clusters w, w + 8, ...)
+// the existing summary (cluster_summary: log-sum-exp, min, max, top-k values
+// from registers) plus the top-k histogram; then every prefix at once.
+// L: scratch for the clusters' top-k lists (where h was staged).
+static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int hn, double *L, csvd_result &res) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const csvd_config &cfg = *D.cfg;
     const int k = cfg.k;
-    const int R = o.cum[hn];
-    __shared__ double s_red[WARPS], s_z[HMAX + 1], s_wl[WARPS * KH];
-    __shared__ int s_hist[HMAX + 2], s_cnt[HMAX + 1];
+    __shared__ double s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX];
+    __shared__ int s_hist[HMAX + 2];
     __shared__ int s_p, s_kind;
-    __shared__ double s_kth;
+    double *s_tk = L;  // per-cluster top-k lists (stride k)
     for (int i = tid; i < HMAX + 2; i += THREADS) s_hist[i] = 0;
-    // ---- the head's logits, contiguous per thread
-    const int i0 = tid * HJ;
-    double v[HJ];
+    __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 52);
+    // top-k histogram: element i counts for every prefix p >= max(q + 1,
+    // 1 + #{p in [1, hn] : Uo[p] >= S_i}) (Uo is non-increasing, Uo[p >= C] = -inf)
+    const int hnu = min(hn, D.C - 1);
+    auto hist_add = [&](double x, int q) {
+        int c = 0;
 #pragma unroll
-    for (int j = 0; j < HJ; j += 2) {
-        if (i0 + j + 1 < R) {
-            const double2 t = __ldcg(reinterpret_cast<const double2 *>(D.S_logits + i0 + j));
-            v[j] = t.x;
-            v[j + 1] = t.y;
+        for (int step = 64; step; step >>= 1)
+            if (c + step <= hnu && o.Uo[c + step] >= x) c += step;
+        const int st = max(q + 1, c + 1);
+        if (st <= hn) atomicAdd(&s_hist[st], 1);
+    };
+#pragma unroll 1
+    for (int q = warp; q < hn; q += WARPS) {
+        const int lo = o.cum[q], hi = o.cum[q + 1];
+        double pre[SUM_E];
+        summary_load(D, lo, hi, pre, lane);
+        if (hi - lo <= 32 * SUM_E) {
+#pragma unroll
+            for (int e = 0; e < SUM_E; ++e)
+                if (lane + 32 * e < hi - lo) hist_add(pre[e], q);
         } else {
-            v[j] = i0 + j < R ? __ldcg(D.S_logits + i0 + j) : -INFINITY;
-            v[j + 1] = -INFINITY;
+#pragma unroll 1
+            for (int i = lo + lane; i < hi; i += 32) hist_add(__ldcg(D.S_logits + i), q);
         }
-    }
-    double m = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < HJ; ++j) m = fmax(m, v[j]);
-    const double M = block_max(m, s_red);  // syncs: s_hist zeroed too
-    // ---- per-position exp(S - M): thread-local inclusive scan, then warp / block
-    double e[HJ], tot = 0.0;
-#pragma unroll
-    for (int j = 0; j < HJ; ++j) {
-        e[j] = i0 + j < R ? exp_nonpos(__dsub_rn(v[j], M)) : 0.0;
-        tot = __dadd_rn(tot, e[j]);
-        e[j] = tot;
-    }
-    double wi = tot;  // warp inclusive scan of thread totals
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const double u = __shfl_up_sync(CSVD_FULL, wi, off);
-        if (lane >= off) wi = __dadd_rn(wi, u);
+        cluster_summary(D, lo, hi, k, s_tk + q * k, s_zq + q, s_mnq + q, s_mxq + q, pre, lane);
     }
     __syncthreads();
-    if (lane == 31) s_red[warp] = wi;
-    // ---- top-k histogram: element i counts for prefixes >= max(q(i) + 1, p0(i))
-    int q = 0;
-    if (i0 < R) {
-        int lo = 0, hi = hn;  // cum[lo] <= i0 < cum[lo+1]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (o.cum[mid] <= i0) lo = mid; else hi = mid;
-        }
-        q = lo;
-    }
-#pragma unroll
-    for (int j = 0; j < HJ; ++j) {
-        const int i = i0 + j;
-        if (i < R) {
-            while (o.cum[q + 1] <= i) ++q;
-            int lo = 1, hi = hn + 1;  // first p in [1, hn] with Uo[p] < S_i, else hn + 1
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if ((mid >= D.C ? -INFINITY : o.Uo[mid]) < v[j]) hi = mid; else lo = mid + 1;
-            }
-            const int st = max(q + 1, lo);
-            if (st <= hn) atomicAdd(&s_hist[st], 1);
-        }
-    }
-    __syncthreads();
-    double base = 0.0;  // exclusive block prefix of this warp
-    for (int w = 0; w < warp; ++w) base = __dadd_rn(base, s_red[w]);
-    const double excl = __dadd_rn(base, __dsub_rn(wi, tot));  // before this thread's first position
-    // Z(p) = inclusive sum at position cum[p] - 1, written by its owner
-    for (int pp = 1; pp <= hn; ++pp) {
-        const int last = o.cum[pp] - 1;
-        if (last >= i0 && last < i0 + HJ) {
-#pragma unroll
-            for (int j = 0; j < HJ; ++j)
-                if (i0 + j == last) s_z[pp] = __dadd_rn(excl, e[j]);
-        }
-    }
-    __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 53);
     // ---- every prefix at once (warp 0: lane l tests p = l + 1 and l + 33)
     if (warp == 0) {
+        // log Z_S(p) = M + log(sum over the first p clusters of exp(lse_q - M))
+        double M = fmax(lane < hn ? s_zq[lane] : -INFINITY, lane + 32 < hn ? s_zq[lane + 32] : -INFINITY);
+        M = warp_max(M);
+        __syncwarp();
+        if (lane < hn) s_zq[lane] = exp_nonpos(__dsub_rn(s_zq[lane], M));
+        if (lane + 32 < hn) s_zq[lane + 32] = exp_nonpos(__dsub_rn(s_zq[lane + 32], M));
+        __syncwarp();
         int carry = 0;
+        double zc = 0.0;
         int first = 0x7fffffff, kind = -1;
-#pragma unroll
+#pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int p = lane + 1 + 32 * h;
             int c = p <= hn ? s_hist[p] : 0;
-#pragma unroll
+            double z = p <= hn ? s_zq[p - 1] : 0.0;
+#pragma unroll 1
             for (int off = 1; off < 32; off <<= 1) {
                 const int u = __shfl_up_sync(CSVD_FULL, c, off);
-                if (lane >= off) c += u;
+                const double w = __shfl_up_sync(CSVD_FULL, z, off);
+                if (lane >= off) {
+                    c += u;
+                    z = __dadd_rn(z, w);
+                }
             }
             c += carry;
+            z = __dadd_rn(z, zc);
             carry = __shfl_sync(CSVD_FULL, c, 31);
+            zc = __shfl_sync(CSVD_FULL, z, 31);
             if (p <= hn) {
-                s_cnt[p] = c;
+                s_zq[p - 1] = z;  // now Z(p): the sum over the first p clusters
                 const long long n = o.cum[p];
-                const double lz = __dadd_rn(M, csvd_log(s_z[p]));
+                const double lz = __dadd_rn(M, csvd_log(z));
                 const double lr = o.lrh[p];
                 int kd = -1;
                 if (n > cfg.k_max) {
@@ -230,7 +205,7 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
                 }
             }
         }
-#pragma unroll
+#pragma unroll 1
         for (int off = 16; off; off >>= 1) {
             const int f2 = __shfl_xor_sync(CSVD_FULL, first, off), k2 = __shfl_xor_sync(CSVD_FULL, kind, off);
             if (f2 < first) {
@@ -238,133 +213,100 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
                 kind = k2;
             }
         }
+        const int ps = first;
+        if (ps <= hn && kind != 99) {
+            // k-th largest over the first ps clusters: k pops over their lists
+            // (lane l holds cluster l and l + 32), then min / max / xi / rho
+            const int n = o.cum[ps];
+            int ha = 0, hb = 0;  // list cursors
+            const int na = lane < ps ? min(k, o.cum[lane + 1] - o.cum[lane]) : 0;
+            const int nb = lane + 32 < ps ? min(k, o.cum[lane + 33] - o.cum[lane + 32]) : 0;
+            double kth = -INFINITY;
+            const int kk = min(k, n);
+#pragma unroll 1
+            for (int r = 0; r < kk; ++r) {
+                const double va = ha < na ? s_tk[lane * k + ha] : -INFINITY;
+                const double vb = hb < nb ? s_tk[(lane + 32) * k + hb] : -INFINITY;
+                const double best = warp_max(fmax(va, vb));
+                const unsigned win = __ballot_sync(CSVD_FULL, va == best || vb == best);
+                if (lane == __ffs(win) - 1) {
+                    if (va == best) ++ha; else ++hb;
+                }
+                kth = best;
+            }
+            double lo = INFINITY, hi = -INFINITY;
+            if (lane < ps) {
+                lo = s_mnq[lane];
+                hi = s_mxq[lane];
+            }
+            if (lane + 32 < ps) {
+                lo = fmin(lo, s_mnq[lane + 32]);
+                hi = fmax(hi, s_mxq[lane + 32]);
+            }
+            lo = warp_min(lo);
+            hi = warp_max(hi);
+            if (lane == 0) {
+                const double lz = __dadd_rn(M, csvd_log(s_zq[ps - 1]));
+                const double lr = o.lrh[ps];
+                const double rho = csvd_rho(lz, lr);
+                const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
+                double xi;
+                if (n < 2 || ps >= D.C) xi = NAN;
+                else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+                double eps_ach = 0.0;
+                if (kind == CSVD_KIND_SOFTMAX_EPS) {
+                    eps_ach = rho;
+                } else if (kind == CSVD_KIND_TOPP_MASS) {
+                    const double dl = csvd_delta(lz, lr);
+                    eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+                }
+                memset(&res, 0, sizeof(res));
+                res.kind = kind;
+                res.fallback = CSVD_FB_NONE;
+                res.sub_size = n;
+                res.clusters_opened = ps;
+                res.heap_pops = ps;
+                res.epsilon_achieved = eps_ach;
+                res.u_max = um;
+                res.topk_min = n >= k ? kth : -INFINITY;
+                res.rho = rho;
+                res.xi = xi;
+            }
+        }
         if (lane == 0) {
-            s_p = first;
+            s_p = ps;
             s_kind = kind;
         }
     }
     __syncthreads();
-    const int ps = s_p, kind = s_kind;
-    if (ps > hn || kind == 99) return 0;
-    // ---- the decision prefix: k-th largest, min, max over positions < cum[ps]
-    const int n = o.cum[ps];
-    double mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < HJ; ++j) {
-        if (i0 + j >= n) v[j] = -INFINITY;
-        else mn = fmin(mn, v[j]);
-        mx = fmax(mx, v[j]);
-    }
-    mn = warp_min(mn);
-    mx = warp_max(mx);
-    // per warp: k pops of the largest remaining value (REDUX on order-preserving keys)
-    const int kk = min(k, n);
-#pragma unroll 1
-    for (int r = 0; r < kk; ++r) {
-        double hd = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < HJ; ++j) hd = fmax(hd, v[j]);
-        const unsigned long long key = dkey(hd);
-        const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
-        const unsigned mh = __reduce_max_sync(CSVD_FULL, kh);
-        const unsigned ml = __reduce_max_sync(CSVD_FULL, kh == mh ? kl : 0u);
-        const unsigned win = __ballot_sync(CSVD_FULL, kh == mh && kl == ml);
-        if (lane == 0) s_wl[warp * KH + r] = dkey_inv(((unsigned long long)mh << 32) | ml);
-        if (lane == __ffs(win) - 1) {
-            bool done = false;
-#pragma unroll
-            for (int j = 0; j < HJ; ++j)
-                if (!done && v[j] == hd) {
-                    v[j] = -INFINITY;
-                    done = true;
-                }
-        }
-    }
-    __shared__ double s_mxw[WARPS];
-    __syncthreads();
-    if (lane == 0) {
-        s_red[warp] = mn;
-        s_mxw[warp] = mx;
-    }
-    if (warp == 0) {
-        // merge the warps' lists: lane l holds the l-th entry of every warp's list
-        double u[WARPS];
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) u[w] = lane < kk ? s_wl[w * KH + lane] : -INFINITY;
-        double kth = -INFINITY;
-#pragma unroll 1
-        for (int r = 0; r < kk; ++r) {
-            double hd = -INFINITY;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) hd = fmax(hd, u[w]);
-            const unsigned long long key = dkey(hd);
-            const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
-            const unsigned mh = __reduce_max_sync(CSVD_FULL, kh);
-            const unsigned ml = __reduce_max_sync(CSVD_FULL, kh == mh ? kl : 0u);
-            const unsigned win = __ballot_sync(CSVD_FULL, kh == mh && kl == ml);
-            kth = dkey_inv(((unsigned long long)mh << 32) | ml);
-            if (lane == __ffs(win) - 1) {
-                bool done = false;
-#pragma unroll
-                for (int w = 0; w < WARPS; ++w)
-                    if (!done && u[w] == hd) {
-                        u[w] = -INFINITY;
-                        done = true;
-                    }
-            }
-        }
-        if (lane == 0) s_kth = n >= k ? kth : -INFINITY;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double lo = s_red[0], hi = s_mxw[0];
-        for (int w = 1; w < WARPS; ++w) {
-            lo = fmin(lo, s_red[w]);
-            hi = fmax(hi, s_mxw[w]);
-        }
-        const double lz = __dadd_rn(M, csvd_log(s_z[ps]));
-        const double lr = o.lrh[ps];
-        const double rho = csvd_rho(lz, lr);
-        const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
-        double xi;
-        if (n < 2 || ps >= D.C) xi = NAN;
-        else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
-        double eps_ach = 0.0;
-        if (kind == CSVD_KIND_SOFTMAX_EPS) {
-            eps_ach = rho;
-        } else if (kind == CSVD_KIND_TOPP_MASS) {
-            const double dl = csvd_delta(lz, lr);
-            eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
-        }
-        memset(&res, 0, sizeof(res));
-        res.kind = kind;
-        res.fallback = CSVD_FB_NONE;
-        res.sub_size = n;
-        res.clusters_opened = ps;
-        res.heap_pops = ps;
-        res.epsilon_achieved = eps_ach;
-        res.u_max = um;
-        res.topk_min = s_kth;
-        res.rho = rho;
-        res.xi = xi;
-    }
-    __syncthreads();
-    return 1;
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 54);
+    return (s_p <= hn && s_kind != 99) ? 1 : 0;
 }
 
-template <typename ET, int Q>
-__global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev D) {
+// The head path; returns true when the step needs the general path (every
+// CTA of the grid / lane returns the same), which the caller then runs from
+// scratch: one call site, so one copy of its code, after the head path's.
+template <typename ET, int Q, bool GROUPED>
+__device__ __forceinline__ bool head_path(const Dev &D) {
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int G = gridDim.x, b = blockIdx.x;
+    const int G = CTA_N, b = CTA_ID;
     double *hs = smem;
     double *ws = smem + D.ord_off;
     double *sws = smem + D.sum_off;
     __shared__ ScanShared ss;
     __shared__ unsigned long long s_hbar, s_epoch;
+    __shared__ double s_qn;
     const bool lead = b == 0 && tid == 0;
     if (lead) DBG_TS(D, 24);
-    if (tid == 0) mbar_init(&s_hbar, 1);
+    if (tid == 0) {
+        mbar_init(&s_hbar, 1);
+        if constexpr (GROUPED) {  // this lane's step number: no grid barrier in a lane
+            unsigned long long e;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(e) : "l"(D.bar64) : "memory");
+            s_epoch = e + 1;
+        }
+    }
     __syncthreads();
     tma_stage_leaves(D.wplan, D.h, D.d, 1, hs, 0, &s_hbar, 0);
     if (b == 1 % G && warp == 0 && lane == 0) {  // per-cluster arrays the head and rows read next
@@ -375,15 +317,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
         bulk_prefetch_l2(D.wrow0, sizeof(int) * D.C);
     }
     if (lead) DBG_TS(D, 25);
-    const double qn = head_bounds<Q>(D, hs);
-    if (lead) {
-        D.res->query_norm = qn;
-        DBG_TS(D, 26);
-    }
-    {
+    if constexpr (GROUPED) {  // batch lane: the dots come from k_bounds_batch, ||h|| here
+        lane_query_norm<Q>(D, hs, s_qn);
+    } else {
+        const double qn = head_bounds<Q>(D, hs);
+        if (lead) {
+            D.res->query_norm = qn;
+            s_qn = qn;
+            DBG_TS(D, 26);
+        }
         const unsigned long long e = grid_sync_mono(D, D.bar64);
         if (tid == 0) s_epoch = e;
+        __syncthreads();
     }
+    const double qn = s_qn;
     if (lead) DBG_TS(D, 27);
     // ---- the head of the opening order (every CTA, identically)
     Ord o;
@@ -391,20 +338,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
     __shared__ double s_slack, s_est;
     const bool ok = stage_bounds(D, o, qn, &s_slack);
     const int hn = ok ? order_head(D, o, s_est) : 0;
-    if (hn == 0 || G < 2) {  // every CTA sees the same: the general step decides
+    if (hn == 0) {  // every CTA sees the same: the general step decides
         __syncthreads();
-        step_body<ET, 8, Q, 8, Q>(D);
-        return;
+        return true;
     }
     if (tid == 0) init_state(D, o, ss, hn, s_est);
     if (lead) DBG_TS(D, 28);
     const unsigned long long epoch = s_epoch;
     unsigned long long *decision = D.bar64 + 1;  // epoch * 2 + decided
     const int R = o.cum[hn];
-    if (b > 0) {
-        // ---- row CTA: rows of the head, contiguous per CTA
-        const int rb = b - 1, Gr = G - 1;
+    const bool solo = G == 1;  // a one-CTA lane computes its rows itself
+    if (b > 0 || solo) {
+        // ---- rows of the head, contiguous per row CTA
+        const int rb = solo ? 0 : b - 1, Gr = solo ? 1 : G - 1;
         const int r_lo = (int)((long long)R * rb / Gr), r_hi = (int)((long long)R * (rb + 1) / Gr);
+#pragma unroll 1
         for (int r = r_lo + warp; r < r_hi; r += WARPS) {
             int lo = 0, hi = hn;  // cum[lo] <= r < cum[lo+1]
             while (hi - lo > 1) {
@@ -423,14 +371,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
         if (lane == 0) __threadfence();
         __syncthreads();
         if (D.dbg && tid == 0) D.dbg[384 + (b & 255)] = gtimer();
-        // this CTA's share of every cluster it touches (release: the rows above are visible first)
-        if (tid < hn) {
-            const int a = max(o.cum[tid], r_lo), e = min(o.cum[tid + 1], r_hi);
-            if (e > a) {
-                __threadfence();
-                atomicAdd(D.hcnt + tid, e - a);
-            }
-        }
         if (D.res_host) {  // host-API step: this CTA's rows into the mapped buffers (speculative:
                            // the host reads only the first |S| entries)
             for (int r = r_lo + tid; r < r_hi; r += THREADS) {
@@ -438,49 +378,67 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
                 D.ids_host[r] = __ldcg(D.S_ids + r);
             }
         }
-        // ---- wait for CTA 0's decision
-        __shared__ int s_dec;
-        if (tid == 0) {
-            unsigned long long v, spins = 0;
+        if (!solo) {
+            // this CTA's share of every cluster it touches, then its arrival
+            // (release: the rows above are visible first)
+            if (tid < hn) {
+                const int a = max(o.cum[tid], r_lo), e = min(o.cum[tid + 1], r_hi);
+                if (e > a) {
+                    __threadfence();
+                    atomicAdd(D.hcnt + tid, e - a);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(D.hcnt + HMAX, 1);
+            }
+            // ---- wait for CTA 0's decision
+            __shared__ int s_dec;
+            if (tid == 0) {
+                unsigned long long v, spins = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(decision) : "memory");
+                    if (++spins > (1ull << 26)) {
+                        D.res->error = CSVD_ESTATE;
+                        v = epoch * 2 + 1;
+                    }
+                } while ((v >> 1) < epoch);
+                s_dec = (int)(v & 1);
+                if (D.dbg && b < 256) D.dbg[128 + b] = gtimer();
+            }
+            __syncthreads();
+            return !s_dec;  // undecided: the general step, from scratch
+        }
+    }
+    // ---- CTA 0: wait for every head cluster's rows and every row CTA, then certify
+    if (!solo) {
+        for (int q = tid; q <= hn; q += THREADS) {
+            const int n = q < hn ? o.cum[q + 1] - o.cum[q] : G - 1;
+            const int *ctr = D.hcnt + (q < hn ? q : HMAX);
+            unsigned long long spins = 0;
+            int v;
             do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(decision) : "memory");
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
                 if (++spins > (1ull << 26)) {
                     D.res->error = CSVD_ESTATE;
-                    v = epoch * 2 + 1;
+                    break;
                 }
-            } while ((v >> 1) < epoch);
-            s_dec = (int)(v & 1);
-            if (D.dbg && b < 256) D.dbg[128 + b] = gtimer();
+            } while (v < n);
         }
         __syncthreads();
-        if (s_dec) return;
-        step_body<ET, 8, Q, 8, Q>(D);  // undecided: the general step, from scratch
-        return;
+        __threadfence();
     }
-    // ---- CTA 0: wait for every head cluster's rows, then certify
-    for (int q = tid; q < hn; q += THREADS) {
-        const int n = o.cum[q + 1] - o.cum[q];
-        unsigned long long spins = 0;
-        int v;
-        do {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(D.hcnt + q) : "memory");
-            if (++spins > (1ull << 26)) {
-                D.res->error = CSVD_ESTATE;
-                break;
-            }
-        } while (v < n);
-    }
-    __syncthreads();
-    __threadfence();
     if (lead) DBG_TS(D, 29);
     __shared__ csvd_result s_res;
     bool decided;
-    if (head_fits(o, hn)) {
-        decided = head_certify(D, o, hn, s_res) != 0;
-    } else {  // more than THREADS * HJ head tokens: per-cluster summaries + the sequential scan
+    if (head_fits(D, o, hn) && D.cfg->k <= KH) {
+        decided = head_certify(D, o, hn, hs, s_res) != 0;
+    } else {  // a head larger than the h staging area: per-cluster summaries + the sequential scan
         const int k = D.cfg->k;
         double *c_vals = sws, *c_lse = sws + 6 * CHUNK, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;
-        double *la = c_max + CHUNK, *lb = la + D.K, *c_topk = lb + D.K;
+        double *la = D.klists ? D.klists + (size_t)CTA_ID * D.klist_stride : c_max + CHUNK;
+        double *lb = la + D.K, *c_topk = lb + D.K;
         double reg_list = -INFINITY;
         for (int q0 = 0; q0 < hn; q0 += D.chunk) {
             const int q1 = min(hn, q0 + D.chunk);
@@ -500,8 +458,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
         __syncthreads();
     }
     if (lead) DBG_TS(D, 31);
-    // every row CTA has added its counts (all head clusters completed): reset
-    for (int q = tid; q < hn; q += THREADS) D.hcnt[q] = 0;
+    // every row CTA has added its counts and arrived: reset
+    for (int q = tid; q <= HMAX; q += THREADS) D.hcnt[q] = 0;
     if (tid == 0) {
         if (decided) {
             csvd_result r = s_res;
@@ -519,10 +477,45 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
             if (D.res_host) *D.res_host = r;
         }
         __threadfence();
+        if constexpr (GROUPED) D.bar64[0] = epoch;  // the lane's step count (read before the next step)
         const unsigned long long w = epoch * 2 + (decided ? 1 : 0);
         asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(decision), "l"(w) : "memory");
         DBG_TS(D, 30);
     }
     __syncthreads();
-    if (!decided) step_body<ET, 8, Q, 8, Q>(D);
+    return !decided;
+}
+
+template <typename ET, int Q>
+__global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev D) {
+    if (head_path<ET, Q, false>(D)) step_body<ET, 8, Q, 8, Q>(D);
+}
+
+// batch lanes: lane b is blockIdx.x / nblocks and swaps its own workspaces
+// into the Dev (all table data is shared); bounds come from k_bounds_batch
+template <typename ET, int Q>
+__global__ void __launch_bounds__(THREADS, 1) k_head_lanes(const __grid_constant__ Dev D0) {
+    Dev D = D0;
+    const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
+    D.h = w.h;
+    D.U = w.U;
+    D.Uraw = w.Uraw;
+    D.dots = w.dots;
+    D.order_g = w.order_g;
+    D.cum_g = w.cum_g;
+    D.S_logits = w.S_logits;
+    D.S_ids = w.S_ids;
+    D.st = w.st;
+    D.res = w.res;
+    D.bar = w.bar;
+    D.cand = w.cand;
+    D.klists = w.klists;
+    D.shard_out = w.shard_out;
+    D.res_host = w.res_host;
+    D.ids_host = w.ids_host;
+    D.logits_host = w.logits_host;
+    D.hcnt = w.hcnt;
+    D.bar64 = w.bar64;
+    D.dbg = nullptr;
+    if (head_path<ET, Q, true>(D)) step_body<ET, 8, Q, 8, Q>(D);
 }

@@ -59,6 +59,8 @@ struct LaneWS {
     csvd_result *res_host;
     long long *ids_host;
     double *logits_host;
+    int *hcnt;                 // head lanes: completion counters [HMAX + 1]
+    unsigned long long *bar64; // head lanes: [0] step count, [1] decision word
 };
 
 struct Dev {
@@ -521,12 +523,13 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = D.C;
     const double *__restrict__ Us = o.Us;
-    double *__restrict__ xs = reinterpret_cast<double *>(o.keys);  // x by cluster id
+    const double *__restrict__ xs = reinterpret_cast<const double *>(o.keys);  // x by cluster id
     __shared__ unsigned long long s_k[WARPS];
-    __shared__ int s_i[WARPS], s_n, s_fail, s_head[64];
+    __shared__ int s_i[WARPS], s_n, s_head[64];
     __shared__ double s_x[WARPS];
-    __shared__ double s_est;
-    // --- top cluster c0
+    __shared__ int s_hz[64], s_hc[64];       // head by position: size, cluster
+    __shared__ double s_he[64], s_hu[64];    // head by position: exp(x - xmax), U
+    // --- top cluster c0: argmin of (okey(U), id); every thread folds the warp results
     unsigned long long bk = ~0ull;
     int bi = 0x7fffffff;
     for (int c = tid; c < C; c += THREADS) {
@@ -549,24 +552,17 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
         s_k[warp] = bk;
         s_i[warp] = bi;
     }
-    if (tid == 0) {
-        s_n = 0;
-        s_fail = 0;
-    }
+    if (tid == 0) s_n = 0;
     __syncthreads();
-    if (tid == 0) {
-        for (int w = 1; w < WARPS; ++w)
-            if (okey_before(s_k[w], s_i[w], bk, bi)) {
-                bk = s_k[w];
-                bi = s_i[w];
-            }
-        s_i[0] = bi;
-        s_est = o.Uo[bi];  // estimate by id (stage_bounds)
-    }
-    __syncthreads();
-    const int c0 = s_i[0];
-    const double est = s_est;
-    if (threadIdx.x == 0) est_out = est;  // init_state's wave estimate, already known here
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w)
+        if (okey_before(s_k[w], s_i[w], bk, bi)) {
+            bk = s_k[w];
+            bi = s_i[w];
+        }
+    const int c0 = bi;
+    const double est = o.Uo[c0];  // the best-logit estimate by id (stage_bounds)
+    if (tid == 0) est_out = est;  // init_state's wave estimate, already known here
     // --- membership, x = log|c| + U (certify.py:119), best non-head cluster
     double xm = -INFINITY;
     bk = ~0ull;
@@ -595,75 +591,65 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
             bi = i2;
         }
     }
-    __syncthreads();  // s_k / s_i reuse
+    __syncthreads();  // s_k / s_i reuse; s_n final
     if (lane == 0) {
         s_k[warp] = bk;
         s_i[warp] = bi;
         s_x[warp] = xm;
     }
-    __syncthreads();
     const int n = s_n;
+    __syncthreads();
     if (n > 64) return 0;
     double xmax = s_x[0];
+#pragma unroll
     for (int w = 1; w < WARPS; ++w) xmax = fmax(xmax, s_x[w]);
-    // --- residual mass of everything outside the head
+    // --- residual mass of everything outside the head; the head's rank by
+    // (key, id) among themselves (thread group of 4 per head element)
     double rest = 0.0;
     for (int c = tid; c < C; c += THREADS)
         if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, exp_nonpos(__dsub_rn(xs[c], xmax)));
+    {
+        const int e = tid >> 2, part = tid & 3;
+        int rank = 0;
+        unsigned long long ke = 0;
+        int ie = 0;
+        if (e < n) {
+            ie = s_head[e];
+            ke = okey(Us[ie]);
+            for (int j = part; j < n; j += 4) {
+                const int ij = s_head[j];
+                rank += okey_before(okey(Us[ij]), ij, ke, ie) ? 1 : 0;
+            }
+        }
+        rank += __shfl_xor_sync(CSVD_FULL, rank, 1);
+        rank += __shfl_xor_sync(CSVD_FULL, rank, 2);
+        if (e < n && part == 0) {
+            s_hc[rank] = ie;
+            s_hu[rank] = Us[ie];
+            s_hz[rank] = o.cum[ie];  // |c| by id (stage_bounds)
+            s_he[rank] = exp_nonpos(__dsub_rn(xs[ie], xmax));
+        }
+    }
     rest = warp_sum(rest);
-    __syncthreads();  // s_x reuse
+    __syncthreads();  // s_x reuse; s_h* complete; every read of the by-id staging is done
     if (lane == 0) s_x[warp] = rest;
     __syncthreads();
+    double S_rest = 0.0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) S_rest = __dadd_rn(S_rest, s_x[w]);
+    __shared__ int s_fail;
     if (warp == 0) {
-        double S_rest = 0.0;
-        for (int w = 0; w < WARPS; ++w) S_rest = __dadd_rn(S_rest, s_x[w]);
         int cn = 0x7fffffff;
         unsigned long long kn = ~0ull;
+#pragma unroll
         for (int w = 0; w < WARPS; ++w)
             if (okey_before(s_k[w], s_i[w], kn, cn)) {
                 kn = s_k[w];
                 cn = s_i[w];
             }
-        // register bitonic sort of the head: lane holds positions lane, lane + 32
-        int ia = lane < n ? s_head[lane] : 0x7fffffff, ib = lane + 32 < n ? s_head[lane + 32] : 0x7fffffff;
-        unsigned long long ka = ia < C ? okey(Us[ia]) : ~0ull, kb = ib < C ? okey(Us[ib]) : ~0ull;
-#pragma unroll 1
-        for (int kk = 2; kk <= 64; kk <<= 1) {
-#pragma unroll 1
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                if (j == 32) {  // a (pos lane) vs b (pos lane+32), ascending (kk == 64)
-                    if (okey_before(kb, ib, ka, ia)) {
-                        const unsigned long long tk = ka;
-                        ka = kb;
-                        kb = tk;
-                        const int ti = ia;
-                        ia = ib;
-                        ib = ti;
-                    }
-                } else {
-                    const bool lower = (lane & j) == 0;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        unsigned long long &k = h ? kb : ka;
-                        int &i = h ? ib : ia;
-                        const int pos = lane + 32 * h;
-                        const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, k, j);
-                        const int i2 = __shfl_xor_sync(CSVD_FULL, i, j);
-                        const bool up = (pos & kk) == 0;
-                        const bool other_first = okey_before(k2, i2, k, i);
-                        if ((lower == up) ? other_first : !other_first) {
-                            k = k2;
-                            i = i2;
-                        }
-                    }
-                }
-            }
-        }
         // positions lane (a) and lane + 32 (b): order, Uo, cum, lrh
-        const int sa = lane < n ? o.cum[ia] : 0, sb = lane + 32 < n ? o.cum[ib] : 0;  // |c| by id
-        __syncwarp();  // cum is rewritten by position below
-        const double ea = lane < n ? exp_nonpos(__dsub_rn(xs[ia], xmax)) : 0.0;
-        const double eb = lane + 32 < n ? exp_nonpos(__dsub_rn(xs[ib], xmax)) : 0.0;
+        const int sa = lane < n ? s_hz[lane] : 0, sb = lane + 32 < n ? s_hz[lane + 32] : 0;
+        const double ea = lane < n ? s_he[lane] : 0.0, eb = lane + 32 < n ? s_he[lane + 32] : 0.0;
         int ca = sa, cb = sb;  // inclusive prefix sums
         double ra = ea, rb = eb;  // inclusive suffix sums
 #pragma unroll
@@ -681,22 +667,19 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
         }
         const int tot_a = __shfl_sync(CSVD_FULL, ca, 31);
         const double tot_b = __shfl_sync(CSVD_FULL, rb, 0);
+        const double ta = __dadd_rn(S_rest, __dadd_rn(ra, tot_b)), tb = __dadd_rn(S_rest, rb);
         int fail = 0;
         if (lane < n) {
-            o.order[lane] = ia;
-            o.Uo[lane] = Us[ia];
+            o.order[lane] = s_hc[lane];
+            o.Uo[lane] = s_hu[lane];
             o.cum[lane] = ca - sa;
-            const double t = __dadd_rn(S_rest, __dadd_rn(ra, tot_b));
-            fail |= !(t > 1e-280);
-            o.lrh[lane] = __dadd_rn(xmax, csvd_log(t));
+            fail |= !(ta > 1e-280);
         }
         if (lane + 32 < n) {
-            o.order[lane + 32] = ib;
-            o.Uo[lane + 32] = Us[ib];
+            o.order[lane + 32] = s_hc[lane + 32];
+            o.Uo[lane + 32] = s_hu[lane + 32];
             o.cum[lane + 32] = tot_a + cb - sb;
-            const double t = __dadd_rn(S_rest, rb);
-            fail |= !(t > 1e-280);
-            o.lrh[lane + 32] = __dadd_rn(xmax, csvd_log(t));
+            fail |= !(tb > 1e-280);
         }
         const int cbt = __shfl_sync(CSVD_FULL, cb, 31);
         if (lane == 0) {
@@ -705,11 +688,13 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
                 o.order[n] = cn;
                 o.Uo[n] = Us[cn];
                 fail |= !(S_rest > 1e-280);
-                o.lrh[n] = __dadd_rn(xmax, csvd_log(S_rest));
-            } else {
-                o.lrh[n] = -INFINITY;
             }
         }
+        // log R-hat after every head prefix (two logs per lane, independent)
+        const double la = lane < n ? csvd_log(ta) : 0.0, lb = lane + 32 < n ? csvd_log(tb) : 0.0;
+        if (lane < n) o.lrh[lane] = __dadd_rn(xmax, la);
+        if (lane + 32 < n) o.lrh[lane + 32] = __dadd_rn(xmax, lb);
+        if (lane == 0) o.lrh[n] = n < C ? __dadd_rn(xmax, csvd_log(S_rest)) : -INFINITY;
         fail = __any_sync(CSVD_FULL, fail);
         if (lane == 0) s_fail = fail;
     }

@@ -13,4 +13,5 @@ template __global__ void k_step<KI_ET, KI_CPL, KI_Q, KI_CPL, KI_Q, true>(const _
 #endif
 #if KI_CPL == 8
 template __global__ void k_head<KI_ET, KI_Q>(const __grid_constant__ Dev);  // the head step
+template __global__ void k_head_lanes<KI_ET, KI_Q>(const __grid_constant__ Dev);  // head step per batch lane
 #endif

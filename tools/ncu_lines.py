@@ -32,8 +32,9 @@ def sass_lines(obj, fn):
         if m:
             cur = f"{os.path.basename(m.group(1))}:{m.group(2)}"
             continue
-        if infn and re.match(r"\s+/\*[0-9a-f]{4,5}\*/", ln):
-            res.append(cur)
+        m = re.match(r"\s+/\*([0-9a-f]{4,7})\*/", ln)
+        if infn and m:
+            res.append((int(m.group(1), 16), cur))
     return res
 
 
@@ -41,10 +42,13 @@ def main():
     rows = list(csv.reader(open(sys.argv[1])))
     h = rows[1]
     data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
-    lines = sass_lines(sys.argv[2], sys.argv[3])
+    sl = sass_lines(sys.argv[2], sys.argv[3])
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    if len(lines) != len(data):
-        print(f"warning: {len(lines)} SASS lines vs {len(data)} profiled instructions", file=sys.stderr)
+    # match by byte offset from the kernel's first instruction (callee
+    # functions listed after the kernel fall outside its offsets: "other")
+    base = int(data[0]["Address"], 16)
+    by_off = dict(sl)
+    lines = [by_off.get(int(d["Address"], 16) - base, "other") for d in data]
     reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 
     def I(x):
