@@ -127,6 +127,9 @@ struct csvd_ctx {
     void (*kbb)(Dev, const double *, int, double *const *, double *const *, csvd_result *, int) = nullptr;
     size_t kbb_smem = 0;
     int kbb_gq = 0;
+    bool kbb2 = false;  // k_bbatch (chain-per-lane batched dots) instead of k_bounds_batch
+    int kbb2_kq = 0;
+    size_t kbb2_smem = 0;
     cudaGraphExec_t g_batch = nullptr;
     int g_batch_B = 0, g_batch_host = 0, g_batch_head = 0;
     csvd_result *res_map_b = nullptr;  // [lanes] mapped
@@ -669,6 +672,15 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         ctx->kbb_smem = hsb * ctx->kbb_gq;
         CK(cudaFuncSetAttribute((const void *)ctx->kbb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ctx->kbb_smem));
+        // chain-per-lane form (k_bbatch): 4 <= NL <= 64 leaves (the slice tree's depth)
+        const int NL = D0.d / D0.bplan.leaf_len;
+        ctx->kbb2_kq = std::min<int>(KBQ, (int)((227 * 1024) / (sizeof(double) * (size_t)D0.d)));
+        ctx->kbb2 = !getenv("CSVD_KBB_OLD") && NL >= 4 && NL <= 64 && (NL & (NL - 1)) == 0 && ctx->kbb2_kq >= 1;
+        if (ctx->kbb2) {
+            ctx->kbb2_smem = sizeof(double) * (size_t)ctx->kbb2_kq * D0.d;
+            CK(cudaFuncSetAttribute((const void *)k_bbatch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ctx->kbb2_smem));
+        }
     }
     {  // per-lane workspace tables for the grouped launch
         auto ws = [](const Dev &L) {
@@ -735,7 +747,11 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io, bool head) {
     if (host_io)
         CK(cudaMemcpyAsync(ctx->d_H, ctx->H_pin, sizeof(double) * B * D0.d, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->d_cfg, ctx->cfg_pin_b, sizeof(csvd_config), cudaMemcpyHostToDevice, s));
-    if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
+    if (ctx->kbb && ctx->kbb2) {  // all B dot vectors at once: clusters x queries register blocks
+        const int ng = (B + ctx->kbb2_kq - 1) / ctx->kbb2_kq;
+        k_bbatch<<<ctx->nsm, THREADS, ctx->kbb2_smem, s>>>(D0, ctx->d_H, B, ctx->d_dots_l, ctx->kbb2_kq, ng);
+        CK(cudaGetLastError());
+    } else if (ctx->kbb) {  // all B bounds vectors at once, each centroid row read once per 4 queries
         ctx->kbb<<<ctx->grid, THREADS, ctx->kbb_smem, s>>>(D0, ctx->d_H, B, ctx->d_Uraw_l, ctx->d_dots_l,
                                                            ctx->d_res_all, ctx->kbb_gq);
         CK(cudaGetLastError());

@@ -1825,6 +1825,124 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// batched bounds, chain-per-lane form (k_bbatch): the same pairwise tree as
+// warp_dot_regular<double, 8, Q> (d = NL leaves of L elements, L % 8 == 0,
+// NL = 2^m >= 4), but a lane owns ONE chain of a leaf (8 lanes per leaf, 4
+// leaves per warp slice) instead of a whole leaf.  A lane then holds one
+// accumulator per (cluster, query) pair, so a warp register-blocks KR
+// clusters x KQ queries: per element step KR centroid loads and KQ staged h
+// reads feed 2*KR*KQ f64 operations (f64-issue-bound rather than latency- or
+// load-bound).  CTA group g stages queries [g*KQ, (g+1)*KQ) in shared memory
+// (layout hs[j][((u*S + i)*4 + leaf)*8 + chain]) and its warps sweep the
+// cluster groups; the groups of one cluster range run concurrently, so a
+// centroid row comes from HBM once and from L2 for the other groups.
+// Combine: chains ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and the 4 leaves of a
+// slice by xor-butterflies, slices by a balanced binary tree (a carry stack),
+// result 0.0 + total: bit-identical to the leaf-per-lane path.
+// ---------------------------------------------------------------------------
+#define KBR 2  // clusters per warp task
+#define KBQ 6  // queries per CTA group (shared memory: KBQ * d doubles)
+#define KBU 4  // element steps per load batch
+static __global__ void __launch_bounds__(THREADS, 1)
+    k_bbatch(Dev D, const double *__restrict__ H, int B, double *const *dots_l, int kq, int ngroups) {
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int d = D.d, L = D.bplan.leaf_len, S = L >> 3, NS = d / (4 * L);  // slices
+    const int per = max(1, (int)gridDim.x / ngroups);  // CTAs per query group
+    const int t = blockIdx.x % per, cpg = per;
+    for (int g = blockIdx.x / per; g < ngroups; g += max(1, (int)gridDim.x / per)) {
+    const int q0 = g * kq, nq = min(kq, B - q0);
+    __syncthreads();  // the previous group's reads of smem are done
+    // stage the group's queries: destination-ordered, gathered from global
+    for (int idx = tid; idx < nq * d; idx += THREADS) {
+        const int j = idx / d, r = idx - j * d;
+        const int u = r / (S * 32), rem = r - u * (S * 32), i = rem >> 5, ln = rem & 31;
+        smem[idx] = __ldg(H + (size_t)(q0 + j) * d + (u * 4 + (ln >> 3)) * L + 8 * i + (ln & 7));
+    }
+    __syncthreads();
+    const int lt = lane >> 3, ch = lane & 7;
+    const int ncg = (D.C + KBR - 1) / KBR;
+    for (int cg = t * WARPS + warp; cg < ncg; cg += cpg * WARPS) {
+        const double *rp[KBR];
+#pragma unroll
+        for (int r = 0; r < KBR; ++r) rp[r] = D.cent + (size_t)min(cg * KBR + r, D.C - 1) * D.bd + lt * L + ch;
+        double stk[KBR][KBQ][5];  // carry stack of the slice tree (NS <= 32)
+#pragma unroll 1
+        for (int u = 0; u < NS; ++u) {
+            double acc[KBR][KBQ];
+            const double *hp = smem + (size_t)u * S * 32 + lane;
+            const int off = u * 4 * L;
+#pragma unroll 1
+            for (int i0 = 0; i0 < S; i0 += KBU) {
+                double x[KBU][KBR];
+#pragma unroll
+                for (int s2 = 0; s2 < KBU; ++s2)
+#pragma unroll
+                    for (int r = 0; r < KBR; ++r) x[s2][r] = i0 + s2 < S ? __ldg(rp[r] + off + 8 * (i0 + s2)) : 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < KBU; ++s2) {
+                    const int i = i0 + s2;
+                    if (i < S) {
+#pragma unroll
+                        for (int j = 0; j < KBQ; ++j) {
+                            if (j < nq) {
+                                const double hv = hp[(size_t)j * d + i * 32];
+#pragma unroll
+                                for (int r = 0; r < KBR; ++r) {
+                                    const double pr = d_mul(x[s2][r], hv);
+                                    acc[r][j] = (i == 0) ? pr : d_add(acc[r][j], pr);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            // chains -> leaf -> slice (xor 1, 2, 4: chains; 8, 16: leaves)
+#pragma unroll
+            for (int r = 0; r < KBR; ++r)
+#pragma unroll
+                for (int j = 0; j < KBQ; ++j) {
+                    double v = acc[r][j];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
+                    // balanced tree over slices: merge with the stored left
+                    // subtrees while the low bits of u are set, then store
+                    bool go = true;
+#pragma unroll
+                    for (int l = 0; l < 5; ++l) {
+                        if (go) {
+                            if ((u >> l) & 1) {
+                                v = d_add(stk[r][j][l], v);
+                            } else {
+                                stk[r][j][l] = v;
+                                go = false;
+                            }
+                        }
+                    }
+                }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < KBR; ++r) {
+                const int c = cg * KBR + r;
+                if (c < D.C)
+#pragma unroll
+                    for (int j = 0; j < KBQ; ++j)
+                        if (j < nq) {
+                            // the root sits at level log2(NS)
+                            double tot = stk[r][j][0];
+#pragma unroll
+                            for (int l = 1; l < 5; ++l)
+                                if ((1 << l) == NS) tot = stk[r][j][l];
+                            dots_l[q0 + j][c] = d_add(0.0, tot);
+                        }
+            }
+        }
+    }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // standalone full-vocabulary GEMV (oracle.dense_logits, oracle.py:33-41): the
 // same exact row dot as the step's fallback, as its own high-occupancy kernel
 // (2 CTAs / 16 warps per SM, <= 128 registers) so more rows are in flight;

@@ -58,3 +58,19 @@ def test_batch_other_bound_modes(mode):
             exp = O.decode_step(T, ix, H[b], cfg)
             assert_outcome(outs[b], _fields(exp), rtol=TRANS_RTOL, where=f"{mode} q{b}",
                            exact_bounds=mode != "spherical")
+
+
+@pytest.mark.parametrize("d,B", [(512, 9), (4096, 13), (8192, 7), (3584, 1)])
+def test_batch_bounds_tree_per_dimension(d, B):
+    """Batched dots (chain-per-lane register blocks, partial query groups,
+    slice trees of depth 0..4) give every query the single-query outcome."""
+    import paper_2511_21702_b200 as P
+    from paper_2511_21702_b200 import workload as wl
+    T = wl.synth_vocab(6000, d, 40, 0.3, 1)
+    ix = wl.fast_index(T, 40, 3)
+    H = np.vstack([wl.generate_queries(B - B // 3, d, "contextual", 7, centroids=ix.centroids),
+                   wl.generate_queries(B // 3, d, "random", 8)])
+    cfg = P.DecodeConfig(k=10)
+    outs = P.decode_step_batch(T, ix, H, cfg)
+    for b in range(B):
+        assert_outcome(outs[b], _fields(O.decode_step(T, ix, H[b], cfg)), rtol=TRANS_RTOL, where=f"d={d} q{b}")
