@@ -492,6 +492,30 @@ def run_ours(a):
         if i >= 3:
             dense_ms.append(s0.elapsed_time(s1))
 
+    # ---- fallback stream: random (non-contextual) queries, which certify only
+    # through the chain (partial expand / relax eps / full vocabulary) ----
+    from paper_2511_21702_b200 import workload as wl
+    qr = wl.generate_queries(12, a.d, "random", 8)
+    hr = torch.from_numpy(np.ascontiguousarray(qr)).to(local)
+    fb_ms, fb_kinds = [], []
+    for i in range(len(qr)):
+        do_flush()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(ext)
+        lib.csvd_step_device(ctx._ctx, hr[i].data_ptr(), ctypes.byref(ccfg), sp)
+        s1.record(ext)
+        torch.cuda.synchronize(local)
+        if i >= 2:
+            fb_ms.append(s0.elapsed_time(s1))
+    fb_outs = [P.decode_step(T, ix, h, cfg) for h in qr[2:]]
+    fb_kinds = [o.fallback_used for o in fb_outs]
+    fallback_stream = {"queries": "random (seed 8)", "steps": len(fb_ms),
+                       "fallback_rate": float(np.mean([k is not None for k in fb_kinds])),
+                       "fallbacks": {str(k): fb_kinds.count(k) for k in set(fb_kinds)},
+                       "ms_per_step": float(np.mean(fb_ms)),
+                       "note": "device-timed steps, L2 flushed before each; the full-vocabulary level is the "
+                               "in-step dense GEMV"}
+
     sharded = None
     if world > 1:
         sharded = run_sharded(a, torch, P, dist, world, rank, T, ix, q)
@@ -562,6 +586,7 @@ def run_ours(a):
         "gpu_launches": K * (1 if a.no_flush else 2),
         "clocks": clk.summary(),
     }
+    line["fallback_stream"] = fallback_stream
     line.update(batched)
     if sharded is not None:
         line["sharded"] = sharded

@@ -337,6 +337,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     ord_bind(D, ws, o);
     __shared__ double s_slack, s_est;
     const bool ok = stage_bounds(D, o, qn, &s_slack);
+    if (lead) DBG_TS(D, 32);
     const int hn = ok ? order_head(D, o, s_est) : 0;
     if (hn == 0) {  // every CTA sees the same: the general step decides
         __syncthreads();
@@ -432,7 +433,13 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     if (lead) DBG_TS(D, 29);
     __shared__ csvd_result s_res;
     bool decided;
-    if (head_fits(D, o, hn) && D.cfg->k <= KH) {
+    const bool fits = head_fits(D, o, hn) && D.cfg->k <= KH;
+    if (lead && D.dbg) {
+        D.dbg[60] = fits ? 1 : 2;
+        D.dbg[61] = hn;
+        D.dbg[62] = o.cum[hn];
+    }
+    if (fits) {
         decided = head_certify(D, o, hn, hs, s_res) != 0;
     } else {  // a head larger than the h staging area: per-cluster summaries + the sequential scan
         const int k = D.cfg->k;

@@ -562,6 +562,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
         }
     const int c0 = bi;
     const double est = o.Uo[c0];  // the best-logit estimate by id (stage_bounds)
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 33);
     if (tid == 0) est_out = est;  // init_state's wave estimate, already known here
     // --- membership, x = log|c| + U (certify.py:119), best non-head cluster
     double xm = -INFINITY;
@@ -599,6 +600,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     }
     const int n = s_n;
     __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 34);
     if (n > 64) return 0;
     double xmax = s_x[0];
 #pragma unroll
@@ -634,6 +636,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     __syncthreads();  // s_x reuse; s_h* complete; every read of the by-id staging is done
     if (lane == 0) s_x[warp] = rest;
     __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 35);
     double S_rest = 0.0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) S_rest = __dadd_rn(S_rest, s_x[w]);
