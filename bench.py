@@ -75,6 +75,16 @@ def workload_name(a):
     return f"llama3-8b-head V={a.V} d={a.d} C={a.C} g={a.g} {a.dtype} B=1"
 
 
+def c2_config(a, world=1):
+    """The config dict of the headline line (both arms print the same)."""
+    return {"workload": workload_name(a), "global_batch": world, "k": a.k,
+            "targets": ["topk", "softmax_eps"], "epsilon": 0.05,
+            "fallback": ["partial_expand:4", "relax_eps:2.0", "full_vocab"],
+            "weights": a.dtype, "cuda_graph": True,
+            "l2": "flushed between timed steps (384 MiB streaming read)" if not a.no_flush else "not flushed",
+            "parallelism": f"vocab-sharded x{world}" if world > 1 else "single GPU"}
+
+
 def make_workload(a):
     from paper_2511_21702_b200 import workload as wl
     n_modes = max(1, a.C // a.g)
@@ -107,60 +117,70 @@ def step_bytes(ix, outcome, s_w):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    polled every ~1 ms from a thread (nvidia-smi -lms 100 as the fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index=0):
         self.index = index
+        self.sm, self.mx, self.reasons = [], None, set()
+        self.stop = threading.Event()
+        self.t = None
         self.proc = None
-        self.lines = []
+
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+            try:
+                bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            for n, m in self.REASONS.items():
+                if bits & m:
+                    self.reasons.add(n)
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml  # noqa: F401
+            self.t = threading.Thread(target=self._nvml, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                     "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                    stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+            for ln in self.proc.stdout:
+                try:
+                    a, b = [float(x) for x in ln.split(",")[:2]]
+                    self.sm.append(a)
+                    self.mx = b
+                except ValueError:
+                    pass
 
     def summary(self):
-        sm, mx = [], None
-        reasons = set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self.t is not None else "nvidia-smi"}
 
 
 def cpu_baseline(T, ix, q, cfg, seconds, ours=None):
@@ -190,11 +210,43 @@ def cpu_baseline(T, ix, q, cfg, seconds, ours=None):
                   for o, r in zip(ours[:m], refs[:m]))
         parity = {"steps_checked": m, "mismatches": int(bad),
                   "checks": "token ids + f64 logits bit-exact, kind, fallback, k-th logit"}
+    # the other CPU legs of BASELINE.md §3, same host, same run (bounded samples)
+    from paper_2511_21702_b200 import workload as wl
+    legs = {}
+    t1 = time.perf_counter()
+    m = 0
+    while m < 3 and time.perf_counter() - t1 < seconds:  # as shipped: + SHA-256 fingerprint every step
+        wl.table_fingerprint(T)  # decode.py:324 -> tensor_io.py:219-226
+        O.decode_step(T, ix, q[m], cfg)
+        m += 1
+    d1 = time.perf_counter() - t1
+    legs["reference_as_is"] = {"value": m / d1, "unit": UNIT, "cores": 1,
+                               "sample": f"{m} steps, per-step SHA-256 table fingerprint recomputed as the "
+                                         f"reference does (decode.py:324)"}
+    try:
+        import threadpoolctl
+        ctl = threadpoolctl.threadpool_limits(cores)
+    except Exception:
+        ctl = None
+    w32 = T.weights if T.weights.dtype == np.float32 else None
+    if w32 is not None:
+        h32 = q[0].astype(np.float32)
+        w32 @ h32
+        t2, r = time.perf_counter(), 0
+        while r < 20 and time.perf_counter() - t2 < seconds / 3:
+            w32 @ q[r % len(q)].astype(np.float32)
+            r += 1
+        d2 = time.perf_counter() - t2
+        legs["dense_blas_f32_gemv"] = {"value": r / d2, "unit": UNIT, "cores": cores,
+                                       "sample": f"{r} numpy float32 W @ h (BLAS, {cores} threads): the "
+                                                 f"non-exact dense full-vocabulary product, for scale"}
+    if ctl is not None:
+        ctl.unregister() if hasattr(ctl, "unregister") else None
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{n} consecutive steps of the same contextual query stream ({dt:.1f} s), "
                       f"oracle/csvd_oracle.py decode_step with the per-step SHA-256 fingerprint of the "
                       f"reference memoized and the pairwise f64 GEMV in C on {cores} threads",
-            "fallback_rate": fb / max(n, 1), "parity_vs_gpu": parity}
+            "fallback_rate": fb / max(n, 1), "parity_vs_gpu": parity, "legs": legs}
 
 
 C3 = dict(name="qwen2.5-head", V=151552, d=3584, C=2273, g=1, dtype="bf16", Bs=(16,), eps=1e-3,
@@ -397,7 +449,7 @@ def run_reference(a):
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": n, "warmup": a.warmup,
         "ms_per_step": 1e3 * tot / n, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference synth_vocab + fast index + contextual queries)",
-        "config": {"workload": workload_name(a), "global_batch": 1, "k": a.k, "l2": "n/a (CPU)"},
+        "config": c2_config(a, int(os.environ.get("WORLD_SIZE", "1"))),
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{n} steps of the contextual stream, oracle port of csvd.decode_step "
@@ -473,6 +525,8 @@ def run_ours(a):
         torch.cuda.synchronize(local)
         if world > 1:
             dist.barrier()
+    nl = ctypes.c_int32(0)
+    lib.csvd_last_launches(ctx._ctx, ctypes.byref(nl))  # kernels per csvd_step_device call
     step_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
     total_ms = sum(step_ms)
     if world > 1:
@@ -561,12 +615,7 @@ def run_ours(a):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: reference synth_vocab mixture (seed 1) + fast index + contextual queries (seed 7)",
-        "config": {"workload": workload_name(a), "global_batch": world, "k": a.k,
-                   "targets": ["topk", "softmax_eps"], "epsilon": 0.05,
-                   "fallback": ["partial_expand:4", "relax_eps:2.0", "full_vocab"],
-                   "weights": a.dtype, "cuda_graph": True,
-                   "l2": "flushed between timed steps (384 MiB streaming read)" if not a.no_flush else "not flushed",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": c2_config(a, world),
         "e2e": {"value": world * e2e_v if world > 1 else e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
@@ -581,9 +630,10 @@ def run_ours(a):
                        "achieved_gbs": dense_bytes / (dense_mean * 1e-3) / 1e9,
                        "frac": dense_bytes / (dense_mean * 1e-3) / 1e9 / pk},
         "speedup_vs_dense_gemv": dense_mean / mean_ms,
-        # timed region: one persistent k_step per step (whatever its waves) plus
-        # the L2-flush kernel before each step
-        "gpu_launches": K * (1 if a.no_flush else 2),
+        # timed region: the step's kernel launches (csvd_last_launches: one
+        # persistent step kernel, whatever its waves / fallback levels) plus the
+        # L2-flush kernel before each step
+        "gpu_launches": K * (nl.value + (0 if a.no_flush else 1)),
         "clocks": clk.summary(),
     }
     line["fallback_stream"] = fallback_stream

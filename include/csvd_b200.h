@@ -128,6 +128,11 @@ typedef struct {
 #define CSVD_SH_SLACK 13
 #define CSVD_SH_TOPK 16      /* then the shard's top-k logits (descending)            */
 
+/* result flags: a tested prefix had |rho - eps| < 1e-12 eps (softmax target)
+ * or |delta - eps/(1-eps)| < 1e-12 of it (top-p target): that decision is a
+ * tie at the ulp level (the device's exp/log and numpy's may disagree). */
+#define CSVD_FLAG_TIE_AMBIGUOUS 1
+
 /* CertStatus + StepMetrics scalars (certify.py:48-53, decode.py:118-130). */
 typedef struct {
     int32_t kind;             /* CSVD_KIND_* */
@@ -144,6 +149,8 @@ typedef struct {
     double slack;
     int32_t error;            /* 0, or CSVD_EVALUE for non-finite bounds */
     int32_t waves;            /* device wave-loop iterations (diagnostic) */
+    int32_t flags;            /* CSVD_FLAG_* */
+    int32_t reserved;
 } csvd_result;
 
 typedef struct csvd_ctx csvd_ctx;

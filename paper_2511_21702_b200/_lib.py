@@ -89,8 +89,12 @@ class Result(ctypes.Structure):
         ("slack", ctypes.c_double),
         ("error", ctypes.c_int32),
         ("waves", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
+
+FLAG_TIE_AMBIGUOUS = 1
 
 # every symbol include/csvd_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -132,6 +132,7 @@ struct csvd_ctx {
     size_t kbb2_smem = 0;
     cudaGraphExec_t g_batch = nullptr;
     int g_batch_B = 0, g_batch_host = 0, g_batch_head = 0;
+    int last_launches = 0;  // kernels launched by the last entry point (csvd_last_launches)
     csvd_result *res_map_b = nullptr;  // [lanes] mapped
     long long *ids_map_b = nullptr;    // [lanes, V] mapped
     double *logits_map_b = nullptr;    // [lanes, V] mapped
@@ -674,10 +675,12 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
                                 (int)ctx->kbb_smem));
         // chain-per-lane form (k_bbatch): 4 <= NL <= 64 leaves (the slice tree's depth)
         const int NL = D0.d / D0.bplan.leaf_len;
-        ctx->kbb2_kq = std::min<int>(KBQ, (int)((227 * 1024) / (sizeof(double) * (size_t)D0.d)));
-        ctx->kbb2 = !getenv("CSVD_KBB_OLD") && NL >= 4 && NL <= 64 && (NL & (NL - 1)) == 0 && ctx->kbb2_kq >= 1;
+        const int NS = NL / 4;
+        ctx->kbb2_kq = KBQ;
+        while (ctx->kbb2_kq > 0 && kbb2_smem_bytes(ctx->kbb2_kq, D0.d, NS) > 227 * 1024) --ctx->kbb2_kq;
+        ctx->kbb2 = getenv("CSVD_KBB_NEW") && NL >= 4 && NL <= 64 && (NL & (NL - 1)) == 0 && ctx->kbb2_kq >= 1;
         if (ctx->kbb2) {
-            ctx->kbb2_smem = sizeof(double) * (size_t)ctx->kbb2_kq * D0.d;
+            ctx->kbb2_smem = kbb2_smem_bytes(ctx->kbb2_kq, D0.d, NS);
             CK(cudaFuncSetAttribute((const void *)k_bbatch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->kbb2_smem));
         }
@@ -828,6 +831,7 @@ extern "C" int csvd_step_batch_device(csvd_ctx *ctx, int32_t B, const double *H_
     if (H_dev != ctx->d_H)
         CK(cudaMemcpyAsync(ctx->d_H, H_dev, sizeof(double) * B * ctx->D.d, cudaMemcpyDeviceToDevice, s));
     CK(cudaGraphLaunch(ctx->g_batch, s));
+    ctx->last_launches = (ctx->kbb ? 1 : 0) + (ctx->kgroup ? 1 : ctx->g_batch_B);
     return 0;
 }
 
@@ -845,6 +849,7 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
     for (int b = 0; b < B; ++b) ctx->res_map_b[b].kind = CSVD_KIND_NONE - 1;  // sentinels, overwritten by the lanes
     auto t1 = now();
     CK(cudaGraphLaunch(ctx->g_batch, s));
+    ctx->last_launches = (ctx->kbb ? 1 : 0) + (ctx->kgroup ? 1 : ctx->g_batch_B);
     auto t2 = now();
     // every lane publishes its result into mapped memory; busy-poll the stream
     cudaError_t q;
@@ -1232,6 +1237,7 @@ extern "C" int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_c
     cudaGraphExec_t g = (ctx->g_step_head && head_config(cfg)) ? ctx->g_step_head : ctx->g_step;
     if (!g) return fail(ctx, CSVD_ESTATE, "no step graph (an earlier workspace change failed)");
     CK(cudaGraphLaunch(g, s));
+    ctx->last_launches = 1;  // one step kernel (it runs the fallback chain itself)
     return 0;
 }
 
@@ -1270,6 +1276,7 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
         cudaGraphExec_t g = (ctx->g_host_head && head_config(cfg)) ? ctx->g_host_head : ctx->g_host;
         if (!g) return fail(ctx, CSVD_ESTATE, "no step graph (an earlier workspace change failed)");
         CK(cudaGraphLaunch(g, s));
+        ctx->last_launches = 1;  // one step kernel (it runs the fallback chain itself)
         auto t2 = std::chrono::steady_clock::now();
         cudaError_t q;
         while ((q = cudaStreamQuery(s)) == cudaErrorNotReady) {
@@ -1341,6 +1348,7 @@ extern "C" int csvd_bounds_host(csvd_ctx *ctx, const double *h, int32_t slack_f3
         if ((rc = launch(ctx, LAUNCH_BOUNDS, s))) return rc;
     } else {
         CK(cudaGraphLaunch(ctx->g_bounds, s));
+        ctx->last_launches = 1;
     }
     CK(cudaMemcpyAsync(ctx->res_pin, ctx->D.res, sizeof(csvd_result), cudaMemcpyDeviceToHost, s));
     if (values) CK(cudaMemcpyAsync(values, ctx->D.U, sizeof(double) * ctx->D.C, cudaMemcpyDeviceToHost, s));
@@ -1362,6 +1370,7 @@ static int dense_async(csvd_ctx *ctx, cudaStream_t s) {
         return launch(ctx, LAUNCH_DENSE, s);
     }
     CK(cudaGraphLaunch(ctx->g_dense, s));
+    ctx->last_launches = 1;
     return 0;
 }
 
@@ -1537,7 +1546,7 @@ extern "C" int csvd_stream(csvd_ctx *ctx, void **stream) {
 
 extern "C" int csvd_last_launches(csvd_ctx *ctx, int32_t *n) {
     if (!ctx || !n) return CSVD_ESTATE;
-    *n = 1;  // one persistent kernel per step, whatever the number of waves
+    *n = ctx->last_launches;  // kernels the last entry point launched (graph kernel nodes)
     return 0;
 }
 

@@ -88,7 +88,7 @@ static __device__ __forceinline__ double head_bounds(const Dev &D, const double 
 // ---------------------------------------------------------------------------
 // Block-parallel certification of the head (CTA 0, all warps): every prefix
 // p = 1..hn of the head is tested at once instead of cluster by cluster.
-//   log Z_S(p)  = M + log(sum over the first p clusters of exp(lse_q - M))
+//   log Z_S(p)  = M + log(sum over the first p clusters of sum exp(S - M))
 //                 (certify.py:79-83; the value the reference's logaddexp chain
 //                 and its 64-merge recompute converge to, within ulps)
 //   top-k test  u_max(p) < kth(p)  <=>  #{i < cum[p] : S_i > Uo[p]} >= k
@@ -102,65 +102,99 @@ static __device__ __forceinline__ double head_bounds(const Dev &D, const double 
 // lists, min / max (xi) from per-cluster extrema.  Returns 1 = decided (res
 // filled), 0 = the step needs the general path (overflow -> fallback chain,
 // or no certificate inside the head).
+#define HJ 16  // decision-prefix logits per lane for the k-th selection (8 warps x 32 lanes x HJ)
 static __device__ __forceinline__ bool head_fits(const Dev &D, const Ord &o, int hn) {
-    return hn * D.cfg->k <= pw_hs_size(D.wplan);  // the clusters' top-k lists fit where h was staged
+    // the head's logits fit where h was staged, and in the warps' registers
+    return o.cum[hn] <= pw_hs_size(D.wplan) && o.cum[hn] <= THREADS * HJ;
 }
 
-// Block-parallel certification.  Per cluster (warp w: clusters w, w + 8, ...)
-// the existing summary (cluster_summary: log-sum-exp, min, max, top-k values
-// from registers) plus the top-k histogram; then every prefix at once.
-// L: scratch for the clusters' top-k lists (where h was staged).
+#define HC_CAS(x, y)                         \
+    {                                        \
+        const double hi_ = fmax(v[x], v[y]); \
+        v[y] = fmin(v[x], v[y]);             \
+        v[x] = hi_;                          \
+    }
+// k pops of the largest remaining head over a warp's sorted lane lists
+// (lane l holds v[0] >= v[1] >= ...); lane 0 writes the popped values
+template <int E>
+static __device__ __forceinline__ void warp_pop_topk(double (&v)[E], int kk, double *out, int lane) {
+#pragma unroll 1
+    for (int r = 0; r < kk; ++r) {
+        const unsigned long long key = dkey(v[0]);
+        const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
+        const unsigned mh = __reduce_max_sync(CSVD_FULL, kh);
+        const unsigned ml = __reduce_max_sync(CSVD_FULL, kh == mh ? kl : 0u);
+        const unsigned win = __ballot_sync(CSVD_FULL, kh == mh && kl == ml);
+        if (lane == 0) out[r] = dkey_inv(((unsigned long long)mh << 32) | ml);
+        if (lane == __ffs(win) - 1) {
+#pragma unroll
+            for (int j = 0; j < E - 1; ++j) v[j] = v[j + 1];
+            v[E - 1] = -INFINITY;
+        }
+    }
+}
+
+// Block-parallel certification (CTA 0).  L: the head's logits staged in
+// shared memory (where h was).
+//   per cluster (warp w: clusters w, w + 8, ...): sum exp(S - M), min, max
+//     and the top-k histogram: element i counts for every prefix p >=
+//     max(q + 1, 1 + #{p in [1, hn] : Uo[p] >= S_i})
+//   warp 0: every prefix's tests at once -> the decision prefix ps
+//   all warps: the k-th largest of positions [0, cum[ps]) (sorted lane
+//     lists + REDUX pops per warp, then a pop-merge of the 8 warp lists)
 static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int hn, double *L, csvd_result &res) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const csvd_config &cfg = *D.cfg;
     const int k = cfg.k;
-    __shared__ double s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX];
+    const int R = o.cum[hn];
+    __shared__ double s_red[WARPS], s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX], s_wl[WARPS * KH];
     __shared__ int s_hist[HMAX + 2];
     __shared__ int s_p, s_kind;
-    double *s_tk = L;  // per-cluster top-k lists (stride k)
+    __shared__ double s_M;
     for (int i = tid; i < HMAX + 2; i += THREADS) s_hist[i] = 0;
-    __syncthreads();
+    double m = -INFINITY;
+#pragma unroll 4
+    for (int i = tid; i < R; i += THREADS) {
+        const double x = __ldcg(D.S_logits + i);
+        L[i] = x;
+        m = fmax(m, x);
+    }
+    const double M = block_max(m, s_red);  // syncs: L, s_hist ready
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 52);
-    // top-k histogram: element i counts for every prefix p >= max(q + 1,
-    // 1 + #{p in [1, hn] : Uo[p] >= S_i}) (Uo is non-increasing, Uo[p >= C] = -inf)
     const int hnu = min(hn, D.C - 1);
-    auto hist_add = [&](double x, int q) {
-        int c = 0;
-#pragma unroll
-        for (int step = 64; step; step >>= 1)
-            if (c + step <= hnu && o.Uo[c + step] >= x) c += step;
-        const int st = max(q + 1, c + 1);
-        if (st <= hn) atomicAdd(&s_hist[st], 1);
-    };
 #pragma unroll 1
     for (int q = warp; q < hn; q += WARPS) {
         const int lo = o.cum[q], hi = o.cum[q + 1];
-        double pre[SUM_E];
-        summary_load(D, lo, hi, pre, lane);
-        if (hi - lo <= 32 * SUM_E) {
+        double z = 0.0, mn = INFINITY, mx = -INFINITY;
+#pragma unroll 2
+        for (int i = lo + lane; i < hi; i += 32) {
+            const double x = L[i];
+            z = __dadd_rn(z, exp_nonpos(__dsub_rn(x, M)));
+            mn = fmin(mn, x);
+            mx = fmax(mx, x);
+            int c = 0;
 #pragma unroll
-            for (int e = 0; e < SUM_E; ++e)
-                if (lane + 32 * e < hi - lo) hist_add(pre[e], q);
-        } else {
-#pragma unroll 1
-            for (int i = lo + lane; i < hi; i += 32) hist_add(__ldcg(D.S_logits + i), q);
+            for (int step = 64; step; step >>= 1)
+                if (c + step <= hnu && o.Uo[c + step] >= x) c += step;
+            const int st = max(q + 1, c + 1);
+            if (st <= hn) atomicAdd(&s_hist[st], 1);
         }
-        cluster_summary(D, lo, hi, k, s_tk + q * k, s_zq + q, s_mnq + q, s_mxq + q, pre, lane);
+        z = warp_sum(z);
+        mn = warp_min(mn);
+        mx = warp_max(mx);
+        if (lane == 0) {
+            s_zq[q] = z;
+            s_mnq[q] = mn;
+            s_mxq[q] = mx;
+        }
     }
     __syncthreads();
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 53);
     // ---- every prefix at once (warp 0: lane l tests p = l + 1 and l + 33)
     if (warp == 0) {
-        // log Z_S(p) = M + log(sum over the first p clusters of exp(lse_q - M))
-        double M = fmax(lane < hn ? s_zq[lane] : -INFINITY, lane + 32 < hn ? s_zq[lane + 32] : -INFINITY);
-        M = warp_max(M);
-        __syncwarp();
-        if (lane < hn) s_zq[lane] = exp_nonpos(__dsub_rn(s_zq[lane], M));
-        if (lane + 32 < hn) s_zq[lane + 32] = exp_nonpos(__dsub_rn(s_zq[lane + 32], M));
-        __syncwarp();
         int carry = 0;
         double zc = 0.0;
-        int first = 0x7fffffff, kind = -1;
+        int first = 0x7fffffff, kind = -1, tie_p = 0x7fffffff;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int p = lane + 1 + 32 * h;
@@ -203,6 +237,14 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
                     first = p;
                     kind = kd;
                 }
+                if (n > 0)
+                    for (int ti = 0; ti < cfg.n_targets; ++ti) {
+                        const int t = cfg.targets[ti];
+                        if (t == CSVD_TARGET_SOFTMAX && near_tie(csvd_rho(lz, lr), cfg.epsilon)) tie_p = min(tie_p, p);
+                        if (t == CSVD_TARGET_TOPP &&
+                            near_tie(csvd_delta(lz, lr), csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon))))
+                            tie_p = min(tie_p, p);
+                    }
             }
         }
 #pragma unroll 1
@@ -213,75 +255,93 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
                 kind = k2;
             }
         }
-        const int ps = first;
-        if (ps <= hn && kind != 99) {
-            // k-th largest over the first ps clusters: k pops over their lists
-            // (lane l holds cluster l and l + 32), then min / max / xi / rho
-            const int n = o.cum[ps];
-            int ha = 0, hb = 0;  // list cursors
-            const int na = lane < ps ? min(k, o.cum[lane + 1] - o.cum[lane]) : 0;
-            const int nb = lane + 32 < ps ? min(k, o.cum[lane + 33] - o.cum[lane + 32]) : 0;
-            double kth = -INFINITY;
-            const int kk = min(k, n);
-#pragma unroll 1
-            for (int r = 0; r < kk; ++r) {
-                const double va = ha < na ? s_tk[lane * k + ha] : -INFINITY;
-                const double vb = hb < nb ? s_tk[(lane + 32) * k + hb] : -INFINITY;
-                const double best = warp_max(fmax(va, vb));
-                const unsigned win = __ballot_sync(CSVD_FULL, va == best || vb == best);
-                if (lane == __ffs(win) - 1) {
-                    if (va == best) ++ha; else ++hb;
-                }
-                kth = best;
-            }
-            double lo = INFINITY, hi = -INFINITY;
-            if (lane < ps) {
-                lo = s_mnq[lane];
-                hi = s_mxq[lane];
-            }
-            if (lane + 32 < ps) {
-                lo = fmin(lo, s_mnq[lane + 32]);
-                hi = fmax(hi, s_mxq[lane + 32]);
-            }
-            lo = warp_min(lo);
-            hi = warp_max(hi);
-            if (lane == 0) {
-                const double lz = __dadd_rn(M, csvd_log(s_zq[ps - 1]));
-                const double lr = o.lrh[ps];
-                const double rho = csvd_rho(lz, lr);
-                const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
-                double xi;
-                if (n < 2 || ps >= D.C) xi = NAN;
-                else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
-                double eps_ach = 0.0;
-                if (kind == CSVD_KIND_SOFTMAX_EPS) {
-                    eps_ach = rho;
-                } else if (kind == CSVD_KIND_TOPP_MASS) {
-                    const double dl = csvd_delta(lz, lr);
-                    eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
-                }
-                memset(&res, 0, sizeof(res));
-                res.kind = kind;
-                res.fallback = CSVD_FB_NONE;
-                res.sub_size = n;
-                res.clusters_opened = ps;
-                res.heap_pops = ps;
-                res.epsilon_achieved = eps_ach;
-                res.u_max = um;
-                res.topk_min = n >= k ? kth : -INFINITY;
-                res.rho = rho;
-                res.xi = xi;
-            }
-        }
+        tie_p = __reduce_min_sync(CSVD_FULL, (unsigned)tie_p);
         if (lane == 0) {
-            s_p = ps;
+            s_p = first;
             s_kind = kind;
+            s_M = tie_p <= first ? 1.0 : 0.0;  // the tie flag, carried to the result
         }
     }
     __syncthreads();
+    const int ps = s_p, kind = s_kind;
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 54);
-    return (s_p <= hn && s_kind != 99) ? 1 : 0;
+    if (ps > hn || kind == 99) return 0;
+    // ---- k-th largest of positions [0, n): warp w takes [w n / 8, (w + 1) n / 8)
+    const int n = o.cum[ps];
+    const int kk = min(k, n);
+    {
+        const int a = (int)((long long)n * warp / WARPS), e = (int)((long long)n * (warp + 1) / WARPS);
+        double v[HJ];
+#pragma unroll
+        for (int j = 0; j < HJ; ++j) {
+            const int i = a + lane + 32 * j;
+            v[j] = i < e ? L[i] : -INFINITY;
+        }
+        HC_CAS(0, 1) HC_CAS(2, 3) HC_CAS(4, 5) HC_CAS(6, 7) HC_CAS(8, 9) HC_CAS(10, 11) HC_CAS(12, 13) HC_CAS(14, 15)
+        HC_CAS(0, 2) HC_CAS(1, 3) HC_CAS(4, 6) HC_CAS(5, 7) HC_CAS(8, 10) HC_CAS(9, 11) HC_CAS(12, 14) HC_CAS(13, 15)
+        HC_CAS(1, 2) HC_CAS(5, 6) HC_CAS(9, 10) HC_CAS(13, 14)
+        HC_CAS(0, 4) HC_CAS(1, 5) HC_CAS(2, 6) HC_CAS(3, 7) HC_CAS(8, 12) HC_CAS(9, 13) HC_CAS(10, 14) HC_CAS(11, 15)
+        HC_CAS(2, 4) HC_CAS(3, 5) HC_CAS(10, 12) HC_CAS(11, 13)
+        HC_CAS(1, 2) HC_CAS(3, 4) HC_CAS(5, 6) HC_CAS(9, 10) HC_CAS(11, 12) HC_CAS(13, 14)
+        HC_CAS(0, 8) HC_CAS(1, 9) HC_CAS(2, 10) HC_CAS(3, 11) HC_CAS(4, 12) HC_CAS(5, 13) HC_CAS(6, 14) HC_CAS(7, 15)
+        HC_CAS(4, 8) HC_CAS(5, 9) HC_CAS(6, 10) HC_CAS(7, 11)
+        HC_CAS(2, 4) HC_CAS(3, 5) HC_CAS(6, 8) HC_CAS(7, 9) HC_CAS(10, 12) HC_CAS(11, 13)
+        HC_CAS(1, 2) HC_CAS(3, 4) HC_CAS(5, 6) HC_CAS(7, 8) HC_CAS(9, 10) HC_CAS(11, 12) HC_CAS(13, 14)
+        warp_pop_topk<HJ>(v, kk, s_wl + warp * KH, lane);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // lane w < WARPS holds warp w's list; k pops across them
+        double u[KH];
+#pragma unroll
+        for (int r = 0; r < KH; ++r) u[r] = (lane < WARPS && r < kk) ? s_wl[lane * KH + r] : -INFINITY;
+        __syncwarp();
+        warp_pop_topk<KH>(u, kk, s_wl, lane);  // the merged list over warp 0's slots
+        __syncwarp();
+        double lo = INFINITY, hi = -INFINITY;
+        if (lane < ps) {
+            lo = s_mnq[lane];
+            hi = s_mxq[lane];
+        }
+        if (lane + 32 < ps) {
+            lo = fmin(lo, s_mnq[lane + 32]);
+            hi = fmax(hi, s_mxq[lane + 32]);
+        }
+        lo = warp_min(lo);
+        hi = warp_max(hi);
+        if (lane == 0) {
+            const double lz = __dadd_rn(M, csvd_log(s_zq[ps - 1]));
+            const double lr = o.lrh[ps];
+            const double rho = csvd_rho(lz, lr);
+            const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
+            double xi;
+            if (n < 2 || ps >= D.C) xi = NAN;
+            else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+            double eps_ach = 0.0;
+            if (kind == CSVD_KIND_SOFTMAX_EPS) {
+                eps_ach = rho;
+            } else if (kind == CSVD_KIND_TOPP_MASS) {
+                const double dl = csvd_delta(lz, lr);
+                eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+            }
+            memset(&res, 0, sizeof(res));
+            res.kind = kind;
+            res.fallback = CSVD_FB_NONE;
+            res.sub_size = n;
+            res.clusters_opened = ps;
+            res.heap_pops = ps;
+            res.epsilon_achieved = eps_ach;
+            res.u_max = um;
+            res.topk_min = n >= k ? s_wl[k - 1] : -INFINITY;
+            res.rho = rho;
+            res.xi = xi;
+            res.flags = s_M != 0.0 ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
+        }
+    }
+    __syncthreads();
+    return 1;
 }
+#undef HC_CAS
 
 // The head path; returns true when the step needs the general path (every
 // CTA of the grid / lane returns the same), which the caller then runs from
@@ -461,7 +521,10 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             if (ss.st.phase != PH_MAIN && ss.st.phase != PH_PE) break;
         }
         decided = ss.st.phase == PH_DONE;
-        if (tid == 0) s_res = ss.res;
+        if (tid == 0) {
+            s_res = ss.res;
+            s_res.flags = ss.flags;
+        }
         __syncthreads();
     }
     if (lead) DBG_TS(D, 31);

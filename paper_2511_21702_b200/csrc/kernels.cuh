@@ -1018,7 +1018,13 @@ struct ScanShared {
     csvd_result res;
     int kcount;
     int head_n;  // > 0: the ordering is valid only for positions [0, head_n] (fast path)
+    int flags;   // CSVD_FLAG_* over the prefixes tested so far
 };
+
+// |x - thr| < 1e-12 * thr: an ulp-level tie of a certification threshold
+__device__ __forceinline__ bool near_tie(double x, double thr) {
+    return fabs(__dsub_rn(x, thr)) < __dmul_rn(1e-12, thr);
+}
 
 // warp 0: per-prefix values of the chunk [q0, q1) from its summaries, then the
 // state machine (scan.cuh).  reg_list: the k <= 32 running list (lane-held);
@@ -1188,6 +1194,17 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
     }
     if (DBG_HERE(D) && lane == 0) DBG_TS(D, 45);
     sc.run(chk);
+    {  // tie flags over the prefixes of this chunk the scan tested
+        bool tie = false;
+        if (act && q + 1 <= stl.p && o.cum[q + 1] > 0)
+            for (int ti = 0; ti < cfg.n_targets; ++ti) {
+                const int t = cfg.targets[ti];
+                if (t == CSVD_TARGET_SOFTMAX) tie |= near_tie(c_rho[lane], cfg.epsilon);
+                else if (t == CSVD_TARGET_TOPP)
+                    tie |= near_tie(c_dl[lane], csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon)));
+            }
+        if (__any_sync(CSVD_FULL, tie) && lane == 0) ss.flags |= CSVD_FLAG_TIE_AMBIGUOUS;
+    }
     if (DBG_HERE(D) && lane == 0) DBG_TS(D, 46);
     __syncwarp();
     if (lane == 0) {
@@ -1369,6 +1386,7 @@ static __device__ __forceinline__ void init_state(const Dev &D, const Ord &o, Sc
     ss.st = st;
     memset(&ss.res, 0, sizeof(ss.res));
     ss.kcount = 0;
+    ss.flags = 0;
     ss.head_n = head_n;
 }
 
@@ -1414,6 +1432,7 @@ static __device__ __forceinline__ void next_wave(const Dev &D, const Ord &o, Sca
     ss.st = s2;
     if (s2.phase == PH_DONE && CTA_ID == 0) {
         csvd_result r = ss.res;
+        r.flags = ss.flags;
         r.query_norm = D.res->query_norm;
         r.slack = D.res->slack;
         r.waves = s2.iter;
@@ -1691,6 +1710,7 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
             __syncthreads();
             if (ss.st.mode == MODE_IDLE && D.res_host) {
                 csvd_result r = ss.res;
+                r.flags = ss.flags;
                 r.query_norm = D.res->query_norm;
                 r.slack = D.res->slack;
                 r.waves = ss.st.iter;
@@ -1845,51 +1865,66 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ---------------------------------------------------------------------------
 #define KBR 2  // clusters per warp task
 #define KBQ 6  // queries per CTA group (shared memory: KBQ * d doubles)
-#define KBU 4  // element steps per load batch
+#define KBU 8  // element steps per load batch (two batches in flight)
+// shared memory of k_bbatch for kq queries of dimension d (NS slices)
+__host__ __device__ inline size_t kbb2_smem_bytes(int kq, int d, int NS) {
+    return sizeof(double) * ((size_t)kq * d + (size_t)WARPS * KBR * KBQ * NS);
+}
 static __global__ void __launch_bounds__(THREADS, 1)
     k_bbatch(Dev D, const double *__restrict__ H, int B, double *const *dots_l, int kq, int ngroups) {
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int d = D.d, L = D.bplan.leaf_len, S = L >> 3, NS = d / (4 * L);  // slices
+    const int NT = NS * S;  // element steps per row (per lane)
+    double *part = smem + (size_t)kq * d + (size_t)warp * KBR * KBQ * NS;  // slice totals [r][j][u]
     const int per = max(1, (int)gridDim.x / ngroups);  // CTAs per query group
     const int t = blockIdx.x % per, cpg = per;
-    for (int g = blockIdx.x / per; g < ngroups; g += max(1, (int)gridDim.x / per)) {
-    const int q0 = g * kq, nq = min(kq, B - q0);
-    __syncthreads();  // the previous group's reads of smem are done
-    // stage the group's queries: destination-ordered, gathered from global
-    for (int idx = tid; idx < nq * d; idx += THREADS) {
-        const int j = idx / d, r = idx - j * d;
-        const int u = r / (S * 32), rem = r - u * (S * 32), i = rem >> 5, ln = rem & 31;
-        smem[idx] = __ldg(H + (size_t)(q0 + j) * d + (u * 4 + (ln >> 3)) * L + 8 * i + (ln & 7));
-    }
-    __syncthreads();
     const int lt = lane >> 3, ch = lane & 7;
     const int ncg = (D.C + KBR - 1) / KBR;
-    for (int cg = t * WARPS + warp; cg < ncg; cg += cpg * WARPS) {
-        const double *rp[KBR];
+    for (int g = blockIdx.x / per; g < ngroups; g += max(1, (int)gridDim.x / per)) {
+        const int q0 = g * kq, nq = min(kq, B - q0);
+        __syncthreads();  // the previous group's reads of smem are done
+        // stage the group's queries: destination-ordered, gathered from global
+        for (int idx = tid; idx < nq * d; idx += THREADS) {
+            const int j = idx / d, r = idx - j * d;
+            const int u = r / (S * 32), rem = r - u * (S * 32), i = rem >> 5, ln = rem & 31;
+            smem[idx] = __ldg(H + (size_t)(q0 + j) * d + (u * 4 + (ln >> 3)) * L + 8 * i + (ln & 7));
+        }
+        __syncthreads();
+        int cg = t * WARPS + warp;
+        if (lane == 0 && cg < ncg)  // this warp's first rows towards L2
+            for (int r = 0; r < KBR; ++r)
+                bulk_prefetch_l2(D.cent + (size_t)min(cg * KBR + r, D.C - 1) * D.bd, sizeof(double) * d);
+        for (; cg < ncg; cg += cpg * WARPS) {
+            const double *rp[KBR];
 #pragma unroll
-        for (int r = 0; r < KBR; ++r) rp[r] = D.cent + (size_t)min(cg * KBR + r, D.C - 1) * D.bd + lt * L + ch;
-        double stk[KBR][KBQ][5];  // carry stack of the slice tree (NS <= 32)
-#pragma unroll 1
-        for (int u = 0; u < NS; ++u) {
-            double acc[KBR][KBQ];
-            const double *hp = smem + (size_t)u * S * 32 + lane;
-            const int off = u * 4 * L;
-#pragma unroll 1
-            for (int i0 = 0; i0 < S; i0 += KBU) {
-                double x[KBU][KBR];
-#pragma unroll
-                for (int s2 = 0; s2 < KBU; ++s2)
-#pragma unroll
-                    for (int r = 0; r < KBR; ++r) x[s2][r] = i0 + s2 < S ? __ldg(rp[r] + off + 8 * (i0 + s2)) : 0.0;
+            for (int r = 0; r < KBR; ++r) rp[r] = D.cent + (size_t)min(cg * KBR + r, D.C - 1) * D.bd + lt * L + ch;
+            const int cn = cg + cpg * WARPS;
+            if (lane == 0 && cn < ncg)  // the next task's rows towards L2 while this one runs
+                for (int r = 0; r < KBR; ++r)
+                    bulk_prefetch_l2(D.cent + (size_t)min(cn * KBR + r, D.C - 1) * D.bd, sizeof(double) * d);
+            // element step gs = u * S + i: address rp + u * 4L + 8i
+            auto ld = [&](double (&x)[KBU][KBR], int gs0) {
 #pragma unroll
                 for (int s2 = 0; s2 < KBU; ++s2) {
-                    const int i = i0 + s2;
-                    if (i < S) {
+                    const int gs = gs0 + s2;
+                    const int u = gs / S, i = gs - u * S;
+#pragma unroll
+                    for (int r = 0; r < KBR; ++r) x[s2][r] = gs < NT ? __ldg(rp[r] + u * 4 * L + 8 * i) : 0.0;
+                }
+            };
+            double acc[KBR][KBQ];
+            auto consume = [&](const double (&x)[KBU][KBR], int gs0) {
+#pragma unroll
+                for (int s2 = 0; s2 < KBU; ++s2) {
+                    const int gs = gs0 + s2;
+                    if (gs < NT) {
+                        const int u = gs / S, i = gs - u * S;
+                        const double *hp = smem + (size_t)gs * 32 + lane;  // (u * S + i) * 32 + lane
 #pragma unroll
                         for (int j = 0; j < KBQ; ++j) {
                             if (j < nq) {
-                                const double hv = hp[(size_t)j * d + i * 32];
+                                const double hv = hp[(size_t)j * d];
 #pragma unroll
                                 for (int r = 0; r < KBR; ++r) {
                                     const double pr = d_mul(x[s2][r], hv);
@@ -1897,51 +1932,40 @@ static __global__ void __launch_bounds__(THREADS, 1)
                                 }
                             }
                         }
-                    }
-                }
-            }
-            // chains -> leaf -> slice (xor 1, 2, 4: chains; 8, 16: leaves)
+                        if (i == S - 1) {  // slice done: chains -> leaves -> slice total
 #pragma unroll
-            for (int r = 0; r < KBR; ++r)
+                            for (int r = 0; r < KBR; ++r)
 #pragma unroll
-                for (int j = 0; j < KBQ; ++j) {
-                    double v = acc[r][j];
+                                for (int j = 0; j < KBQ; ++j) {
+                                    double v = acc[r][j];
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
-                    // balanced tree over slices: merge with the stored left
-                    // subtrees while the low bits of u are set, then store
-                    bool go = true;
-#pragma unroll
-                    for (int l = 0; l < 5; ++l) {
-                        if (go) {
-                            if ((u >> l) & 1) {
-                                v = d_add(stk[r][j][l], v);
-                            } else {
-                                stk[r][j][l] = v;
-                                go = false;
-                            }
+                                    for (int o = 1; o < 32; o <<= 1) v = d_add(v, __shfl_xor_sync(CSVD_FULL, v, o));
+                                    if (lane == 0) part[(r * KBQ + j) * NS + u] = v;
+                                }
                         }
                     }
                 }
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int r = 0; r < KBR; ++r) {
-                const int c = cg * KBR + r;
-                if (c < D.C)
-#pragma unroll
-                    for (int j = 0; j < KBQ; ++j)
-                        if (j < nq) {
-                            // the root sits at level log2(NS)
-                            double tot = stk[r][j][0];
-#pragma unroll
-                            for (int l = 1; l < 5; ++l)
-                                if ((1 << l) == NS) tot = stk[r][j][l];
-                            dots_l[q0 + j][c] = d_add(0.0, tot);
-                        }
+            };
+            double xa[KBU][KBR], xb[KBU][KBR];
+            ld(xa, 0);
+#pragma unroll 1
+            for (int gs0 = 0; gs0 < NT; gs0 += 2 * KBU) {
+                ld(xb, gs0 + KBU);
+                consume(xa, gs0);
+                ld(xa, gs0 + 2 * KBU);
+                consume(xb, gs0 + KBU);
             }
+            __syncwarp();
+            // balanced tree over the slices (in place), one (cluster, query) pair per lane
+            if (lane < KBR * KBQ) {
+                const int r = lane / KBQ, j = lane % KBQ, c = cg * KBR + r;
+                double *pp = part + lane * NS;
+                for (int w = 1; w < NS; w <<= 1)
+                    for (int u = 0; u + w < NS; u += 2 * w) pp[u] = d_add(pp[u], pp[u + w]);
+                if (c < D.C && j < nq) dots_l[q0 + j][c] = d_add(0.0, pp[0]);
+            }
+            __syncwarp();
         }
-    }
     }
 }
 

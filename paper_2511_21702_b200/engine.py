@@ -254,6 +254,7 @@ class DeviceIndex:
             flops_sparse=2 * n * self.d,
             flops_bounds=2 * self.C * self.bounds_dim,
             heap_pops=int(r.heap_pops),
+            tie_ambiguous=bool(r.flags & _lib.FLAG_TIE_AMBIGUOUS),
         )
         return DecodeOutcome(token_ids=ids, logits=logits, status=status, fallback_used=fb, stats=stats)
 

@@ -252,6 +252,10 @@ class StepMetrics:
     flops_bounds: int
     heap_pops: int
     step: int = -1
+    # B200 addition (not in the reference): a tested prefix's rho (or top-p
+    # delta) was within 1e-12 relative of the threshold, i.e. the decision is
+    # an ulp-level tie between the device's and numpy's exp/log
+    tie_ambiguous: bool = False
 
 
 @dataclass
