@@ -9,7 +9,7 @@ imports this module; its CUDA path fails loudly when its extension is absent.
 Parity pinning: this restatement is checked bit-for-bit against outputs of
 the reference itself (imported from /root/reference in the build container)
 by `tests/golden/make_golden.py` -> `tests/golden/*.npz`, and against the
-reference's own known-answer tests (restated in tests/test_oracle_kat.py).
+reference's own known-answer tests (restated in tests/test_kat.py, run on the oracle and the GPU).
 
 Arithmetic is numpy float64 in the reference's order; the row reductions go
 through the C restatement in `oracle/pairwise.c` (multi-threaded, bit-equal to

@@ -102,52 +102,26 @@ static __device__ __forceinline__ double head_bounds(const Dev &D, const double 
 // lists, min / max (xi) from per-cluster extrema.  Returns 1 = decided (res
 // filled), 0 = the step needs the general path (overflow -> fallback chain,
 // or no certificate inside the head).
-#define HJ 16  // decision-prefix logits per lane for the k-th selection (8 warps x 32 lanes x HJ)
 static __device__ __forceinline__ bool head_fits(const Dev &D, const Ord &o, int hn) {
-    // the head's logits fit where h was staged, and in the warps' registers
-    return o.cum[hn] <= pw_hs_size(D.wplan) && o.cum[hn] <= THREADS * HJ;
-}
-
-#define HC_CAS(x, y)                         \
-    {                                        \
-        const double hi_ = fmax(v[x], v[y]); \
-        v[y] = fmin(v[x], v[y]);             \
-        v[x] = hi_;                          \
-    }
-// k pops of the largest remaining head over a warp's sorted lane lists
-// (lane l holds v[0] >= v[1] >= ...); lane 0 writes the popped values
-template <int E>
-static __device__ __forceinline__ void warp_pop_topk(double (&v)[E], int kk, double *out, int lane) {
-#pragma unroll 1
-    for (int r = 0; r < kk; ++r) {
-        const unsigned long long key = dkey(v[0]);
-        const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
-        const unsigned mh = __reduce_max_sync(CSVD_FULL, kh);
-        const unsigned ml = __reduce_max_sync(CSVD_FULL, kh == mh ? kl : 0u);
-        const unsigned win = __ballot_sync(CSVD_FULL, kh == mh && kl == ml);
-        if (lane == 0) out[r] = dkey_inv(((unsigned long long)mh << 32) | ml);
-        if (lane == __ffs(win) - 1) {
-#pragma unroll
-            for (int j = 0; j < E - 1; ++j) v[j] = v[j + 1];
-            v[E - 1] = -INFINITY;
-        }
-    }
+    // the head's logits and its clusters' top-k lists fit where h was staged
+    return o.cum[hn] + hn * D.cfg->k <= pw_hs_size(D.wplan);
 }
 
 // Block-parallel certification (CTA 0).  L: the head's logits staged in
 // shared memory (where h was).
 //   per cluster (warp w: clusters w, w + 8, ...): sum exp(S - M), min, max
 //     and the top-k histogram: element i counts for every prefix p >=
-//     max(q + 1, 1 + #{p in [1, hn] : Uo[p] >= S_i})
-//   warp 0: every prefix's tests at once -> the decision prefix ps
-//   all warps: the k-th largest of positions [0, cum[ps]) (sorted lane
-//     lists + REDUX pops per warp, then a pop-merge of the 8 warp lists)
+//     max(q + 1, 1 + #{p in [1, hn] : Uo[p] >= S_i}), and the cluster's
+//     top-k values (k pops of the lanes' running maxima)
+//   warp 0: every prefix's tests at once -> the decision prefix ps, whose
+//     k-th value is a k-pop merge of the first ps clusters' lists
 static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int hn, double *L, csvd_result &res) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const csvd_config &cfg = *D.cfg;
     const int k = cfg.k;
     const int R = o.cum[hn];
-    __shared__ double s_red[WARPS], s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX], s_wl[WARPS * KH];
+    __shared__ double s_red[WARPS], s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX];
+    double *s_tk = L + R;  // per-cluster top-k lists (stride k), after the logits
     __shared__ int s_hist[HMAX + 2];
     __shared__ int s_p, s_kind;
     __shared__ double s_M;
@@ -182,6 +156,33 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
         z = warp_sum(z);
         mn = warp_min(mn);
         mx = warp_max(mx);
+        // top-k values of the cluster: k pops of the lanes' running maxima
+        const int kk = min(k, hi - lo);
+        double cm = -INFINITY;
+        int ci = -1;
+#pragma unroll 1
+        for (int i = lo + lane; i < hi; i += 32)
+            if (L[i] > cm) {
+                cm = L[i];
+                ci = i;
+            }
+#pragma unroll 1
+        for (int r = 0; r < kk; ++r) {
+            const double best = warp_max(cm);
+            const unsigned win = __ballot_sync(CSVD_FULL, cm == best);
+            if (lane == 0) s_tk[q * k + r] = best;
+            if (lane == __ffs(win) - 1) {  // the winner drops its maximum and rescans
+                L[ci] = -INFINITY;
+                cm = -INFINITY;
+                ci = -1;
+                for (int i = lo + lane; i < hi; i += 32)
+                    if (L[i] > cm) {
+                        cm = L[i];
+                        ci = i;
+                    }
+            }
+            __syncwarp();
+        }
         if (lane == 0) {
             s_zq[q] = z;
             s_mnq[q] = mn;
@@ -266,38 +267,26 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
     const int ps = s_p, kind = s_kind;
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 54);
     if (ps > hn || kind == 99) return 0;
-    // ---- k-th largest of positions [0, n): warp w takes [w n / 8, (w + 1) n / 8)
     const int n = o.cum[ps];
     const int kk = min(k, n);
-    {
-        const int a = (int)((long long)n * warp / WARPS), e = (int)((long long)n * (warp + 1) / WARPS);
-        double v[HJ];
-#pragma unroll
-        for (int j = 0; j < HJ; ++j) {
-            const int i = a + lane + 32 * j;
-            v[j] = i < e ? L[i] : -INFINITY;
-        }
-        HC_CAS(0, 1) HC_CAS(2, 3) HC_CAS(4, 5) HC_CAS(6, 7) HC_CAS(8, 9) HC_CAS(10, 11) HC_CAS(12, 13) HC_CAS(14, 15)
-        HC_CAS(0, 2) HC_CAS(1, 3) HC_CAS(4, 6) HC_CAS(5, 7) HC_CAS(8, 10) HC_CAS(9, 11) HC_CAS(12, 14) HC_CAS(13, 15)
-        HC_CAS(1, 2) HC_CAS(5, 6) HC_CAS(9, 10) HC_CAS(13, 14)
-        HC_CAS(0, 4) HC_CAS(1, 5) HC_CAS(2, 6) HC_CAS(3, 7) HC_CAS(8, 12) HC_CAS(9, 13) HC_CAS(10, 14) HC_CAS(11, 15)
-        HC_CAS(2, 4) HC_CAS(3, 5) HC_CAS(10, 12) HC_CAS(11, 13)
-        HC_CAS(1, 2) HC_CAS(3, 4) HC_CAS(5, 6) HC_CAS(9, 10) HC_CAS(11, 12) HC_CAS(13, 14)
-        HC_CAS(0, 8) HC_CAS(1, 9) HC_CAS(2, 10) HC_CAS(3, 11) HC_CAS(4, 12) HC_CAS(5, 13) HC_CAS(6, 14) HC_CAS(7, 15)
-        HC_CAS(4, 8) HC_CAS(5, 9) HC_CAS(6, 10) HC_CAS(7, 11)
-        HC_CAS(2, 4) HC_CAS(3, 5) HC_CAS(6, 8) HC_CAS(7, 9) HC_CAS(10, 12) HC_CAS(11, 13)
-        HC_CAS(1, 2) HC_CAS(3, 4) HC_CAS(5, 6) HC_CAS(7, 8) HC_CAS(9, 10) HC_CAS(11, 12) HC_CAS(13, 14)
-        warp_pop_topk<HJ>(v, kk, s_wl + warp * KH, lane);
-    }
-    __syncthreads();
     if (warp == 0) {
-        // lane w < WARPS holds warp w's list; k pops across them
-        double u[KH];
-#pragma unroll
-        for (int r = 0; r < KH; ++r) u[r] = (lane < WARPS && r < kk) ? s_wl[lane * KH + r] : -INFINITY;
-        __syncwarp();
-        warp_pop_topk<KH>(u, kk, s_wl, lane);  // the merged list over warp 0's slots
-        __syncwarp();
+        // k-th largest over the first ps clusters: k pops over their lists
+        // (lane l holds cluster l and l + 32)
+        int ha = 0, hb = 0;  // list cursors
+        const int na = lane < ps ? min(k, o.cum[lane + 1] - o.cum[lane]) : 0;
+        const int nb = lane + 32 < ps ? min(k, o.cum[lane + 33] - o.cum[lane + 32]) : 0;
+        double kth = -INFINITY;
+#pragma unroll 1
+        for (int r = 0; r < kk; ++r) {
+            const double va = ha < na ? s_tk[lane * k + ha] : -INFINITY;
+            const double vb = hb < nb ? s_tk[(lane + 32) * k + hb] : -INFINITY;
+            const double best = warp_max(fmax(va, vb));
+            const unsigned win = __ballot_sync(CSVD_FULL, va == best || vb == best);
+            if (lane == __ffs(win) - 1) {
+                if (va == best) ++ha; else ++hb;
+            }
+            kth = best;
+        }
         double lo = INFINITY, hi = -INFINITY;
         if (lane < ps) {
             lo = s_mnq[lane];
@@ -332,7 +321,7 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
             res.heap_pops = ps;
             res.epsilon_achieved = eps_ach;
             res.u_max = um;
-            res.topk_min = n >= k ? s_wl[k - 1] : -INFINITY;
+            res.topk_min = n >= k ? kth : -INFINITY;
             res.rho = rho;
             res.xi = xi;
             res.flags = s_M != 0.0 ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
@@ -341,7 +330,6 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
     __syncthreads();
     return 1;
 }
-#undef HC_CAS
 
 // The head path; returns true when the step needs the general path (every
 // CTA of the grid / lane returns the same), which the caller then runs from
@@ -457,14 +445,20 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             // ---- wait for CTA 0's decision
             __shared__ int s_dec;
             if (tid == 0) {
+                // relaxed polls with a back-off (147 CTAs polling one line must
+                // not crowd L2 while CTA 0 works), one acquire fence at the end
                 unsigned long long v, spins = 0;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(decision) : "memory");
-                    if (++spins > (1ull << 26)) {
+                while (true) {
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(decision) : "memory");
+                    if ((v >> 1) >= epoch) break;
+                    if (++spins > (1ull << 24)) {
                         D.res->error = CSVD_ESTATE;
                         v = epoch * 2 + 1;
+                        break;
                     }
-                } while ((v >> 1) < epoch);
+                    __nanosleep(256);
+                }
+                __threadfence();
                 s_dec = (int)(v & 1);
                 if (D.dbg && b < 256) D.dbg[128 + b] = gtimer();
             }
@@ -480,7 +474,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             unsigned long long spins = 0;
             int v;
             do {
-                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
                 if (++spins > (1ull << 26)) {
                     D.res->error = CSVD_ESTATE;
                     break;
