@@ -494,6 +494,12 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         D.dbg[62] = o.cum[hn];
     }
     if (fits) {
+        if (D.dbg) {  // debug runs: certify twice, timing the warm repeat (slots 55, 56)
+            head_certify(D, o, hn, hs, s_res);
+            if (lead) DBG_TS(D, 55);
+            head_certify(D, o, hn, hs, s_res);
+            if (lead) DBG_TS(D, 56);
+        }
         decided = head_certify(D, o, hn, hs, s_res) != 0;
     } else {  // a head larger than the h staging area: per-cluster summaries + the sequential scan
         const int k = D.cfg->k;

@@ -20,7 +20,7 @@ lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
 names = {24: "kernel start", 25: "h staged", 26: "cta0 bounds done", 27: "barrier passed", 28: "head done (cta0)",
-         29: "cta0: head rows complete", 31: "cta0: certified", 30: "decision published", 32: "stage_bounds", 33: "order: top cluster", 34: "order: membership", 35: "order: rest + rank", 52: "cert: start", 53: "cert: per-cluster pass", 54: "cert: prefixes + k-th", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
+         29: "cta0: head rows complete", 31: "cta0: certified", 30: "decision published", 32: "stage_bounds", 33: "order: top cluster", 34: "order: membership", 35: "order: rest + rank", 55: "cert run 1 (cold) done", 56: "cert run 2 (warm) done", 52: "cert: start", 53: "cert: per-cluster pass", 54: "cert: prefixes + k-th", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
          42: "scan: 64-merge recompute", 43: "scan: k-th merges", 44: "scan: rho/delta", 45: "scan: ballot+merge",
          46: "scan: state machine", 48: "summary: min/max", 49: "summary: warp min/max", 50: "summary: lse",
          51: "summary: sort"}
