@@ -331,6 +331,244 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
     return 1;
 }
 
+// Fast certification for the common case (CTA 0): the decision is the last
+// head prefix p = hn, or an earlier prefix by a softmax / top-p target.
+//   per cluster: sum exp(S - M), min, max only (no per-cluster lists)
+//   kth_all = k-th largest of the whole head (sorted lane lists of 2 x 8 +
+//     REDUX pops per warp, then a pop-merge of the warp lists)
+//   top-k at p < hn cannot certify when kth_all <= Uo[p]: kth(p) <= kth_all
+//     (the prefix's k-th value is non-decreasing in p).  When kth_all >
+//     Uo[p] for some p < hn with the top-k target, or the decision is a p < hn
+//     (its own k-th needed), return -1: head_certify (per-cluster lists and
+//     the histogram) decides instead.
+// Returns 1 decided, 0 general path, -1 use head_certify.
+#define HF_CAS(a, x, y)                      \
+    {                                        \
+        const double hi_ = fmax(a[x], a[y]); \
+        a[y] = fmin(a[x], a[y]);             \
+        a[x] = hi_;                          \
+    }
+#define HF_SORT8(a)                                                               \
+    HF_CAS(a, 0, 1) HF_CAS(a, 2, 3) HF_CAS(a, 4, 5) HF_CAS(a, 6, 7) HF_CAS(a, 0, 2) \
+    HF_CAS(a, 1, 3) HF_CAS(a, 4, 6) HF_CAS(a, 5, 7) HF_CAS(a, 1, 2) HF_CAS(a, 5, 6) \
+    HF_CAS(a, 0, 4) HF_CAS(a, 3, 7) HF_CAS(a, 1, 5) HF_CAS(a, 2, 6) HF_CAS(a, 1, 4) \
+    HF_CAS(a, 3, 6) HF_CAS(a, 2, 4) HF_CAS(a, 3, 5) HF_CAS(a, 3, 4)
+static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o, int hn, double *L,
+                                                     csvd_result &res) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const csvd_config &cfg = *D.cfg;
+    const int k = cfg.k;
+    const int R = o.cum[hn];
+    __shared__ double s_red[WARPS], s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX], s_wl[WARPS * KH];
+    __shared__ int s_p, s_kind;
+    __shared__ double s_kth, s_tie;
+    double m = -INFINITY;
+#pragma unroll 4
+    for (int i = tid; i < R; i += THREADS) {
+        const double x = __ldcg(D.S_logits + i);
+        L[i] = x;
+        m = fmax(m, x);
+    }
+    const double M = block_max(m, s_red);  // syncs: L ready
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 52);
+    // ---- per cluster: exp sums and extrema
+#pragma unroll 1
+    for (int q = warp; q < hn; q += WARPS) {
+        const int lo = o.cum[q], hi = o.cum[q + 1];
+        double z = 0.0, mn = INFINITY, mx = -INFINITY;
+#pragma unroll 4
+        for (int i = lo + lane; i < hi; i += 32) {
+            const double x = L[i];
+            z = __dadd_rn(z, exp_nonpos(__dsub_rn(x, M)));
+            mn = fmin(mn, x);
+            mx = fmax(mx, x);
+        }
+        z = warp_sum(z);
+        mn = warp_min(mn);
+        mx = warp_max(mx);
+        if (lane == 0) {
+            s_zq[q] = z;
+            s_mnq[q] = mn;
+            s_mxq[q] = mx;
+        }
+    }
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 55);
+    // ---- the head's top-k: warp w's slice [w R / 8, (w + 1) R / 8), 2 x 8 per lane
+    const int kk = min(k, R);
+    {
+        const int a0 = (int)((long long)R * warp / WARPS), e0 = (int)((long long)R * (warp + 1) / WARPS);
+        double va[8], vb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = a0 + lane + 32 * j, i2 = i + 256;
+            va[j] = i < e0 ? L[i] : -INFINITY;
+            vb[j] = i2 < e0 ? L[i2] : -INFINITY;
+        }
+        HF_SORT8(va)
+        HF_SORT8(vb)
+        if (DBG_HERE(D) && tid == 0) DBG_TS(D, 56);
+#pragma unroll 1
+        for (int r = 0; r < kk; ++r) {
+            const double hd = fmax(va[0], vb[0]);
+            const unsigned long long key = dkey(hd);
+            const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
+            const unsigned mh = __reduce_max_sync(CSVD_FULL, kh);
+            const unsigned ml = __reduce_max_sync(CSVD_FULL, kh == mh ? kl : 0u);
+            const unsigned win = __ballot_sync(CSVD_FULL, kh == mh && kl == ml);
+            if (lane == 0) s_wl[warp * KH + r] = dkey_inv(((unsigned long long)mh << 32) | ml);
+            if (lane == __ffs(win) - 1) {
+                if (va[0] >= vb[0]) {
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) va[j] = va[j + 1];
+                    va[7] = -INFINITY;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) vb[j] = vb[j + 1];
+                    vb[7] = -INFINITY;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 53);
+    if (warp == 0) {
+        // k-th of the head: k pops over the 8 warp lists (lane w < 8: list w, cursor)
+        int hc = 0;
+        double kth = -INFINITY;
+#pragma unroll 1
+        for (int r = 0; r < kk; ++r) {
+            const double v = (lane < WARPS && hc < kk) ? s_wl[lane * KH + hc] : -INFINITY;
+            const double best = warp_max(v);
+            const unsigned win = __ballot_sync(CSVD_FULL, v == best && lane < WARPS && hc < kk);
+            if (lane == __ffs(win) - 1) ++hc;
+            kth = best;
+        }
+        const double kth_all = R >= k ? kth : -INFINITY;
+        if (DBG_HERE(D) && lane == 0) DBG_TS(D, 58);
+        // every prefix at once: lane l tests p = l + 1 and l + 33
+        double zc = 0.0;
+        int first = 0x7fffffff, kind = -1, tie_p = 0x7fffffff, unsure = 0x7fffffff;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int p = lane + 1 + 32 * h;
+            double z = p <= hn ? s_zq[p - 1] : 0.0;
+#pragma unroll 1
+            for (int off = 1; off < 32; off <<= 1) {
+                const double w = __shfl_up_sync(CSVD_FULL, z, off);
+                if (lane >= off) z = __dadd_rn(z, w);
+            }
+            z = __dadd_rn(z, zc);
+            zc = __shfl_sync(CSVD_FULL, z, 31);
+            if (p <= hn) {
+                s_zq[p - 1] = z;  // Z(p)
+                const long long n = o.cum[p];
+                const double lz = __dadd_rn(M, csvd_log(z));
+                const double lr = o.lrh[p];
+                int kd = -1;
+                if (n > cfg.k_max) {
+                    kd = 99;
+                } else {
+                    for (int ti = 0; ti < cfg.n_targets && kd < 0; ++ti) {
+                        const int t = cfg.targets[ti];
+                        if (t == CSVD_TARGET_TOPK) {
+                            if (n >= k) {
+                                const double u = p >= D.C ? -INFINITY : o.Uo[p];
+                                if (p == hn) {
+                                    if (kth_all > u) kd = CSVD_KIND_TOPK_EXACT;
+                                } else if (kth_all > u) {
+                                    kd = 98;  // kth(p) unknown here: the full certifier decides
+                                }
+                            }
+                        } else if (t == CSVD_TARGET_SOFTMAX) {
+                            if (n > 0 && csvd_rho(lz, lr) <= cfg.epsilon) kd = CSVD_KIND_SOFTMAX_EPS;
+                        } else if (n > 0 && csvd_delta(lz, lr) <= csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon))) {
+                            kd = CSVD_KIND_TOPP_MASS;
+                        }
+                    }
+                }
+                if (kd >= 0 && p < first) {
+                    first = p;
+                    kind = kd;
+                }
+                if (n > 0)
+                    for (int ti = 0; ti < cfg.n_targets; ++ti) {
+                        const int t = cfg.targets[ti];
+                        if (t == CSVD_TARGET_SOFTMAX && near_tie(csvd_rho(lz, lr), cfg.epsilon)) tie_p = min(tie_p, p);
+                        if (t == CSVD_TARGET_TOPP &&
+                            near_tie(csvd_delta(lz, lr), csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon))))
+                            tie_p = min(tie_p, p);
+                    }
+            }
+        }
+#pragma unroll 1
+        for (int off = 16; off; off >>= 1) {
+            const int f2 = __shfl_xor_sync(CSVD_FULL, first, off), k2 = __shfl_xor_sync(CSVD_FULL, kind, off);
+            if (f2 < first) {
+                first = f2;
+                kind = k2;
+            }
+        }
+        tie_p = __reduce_min_sync(CSVD_FULL, (unsigned)tie_p);
+        if (lane == 0) {
+            s_p = first;
+            s_kind = kind;
+            s_kth = kth_all;
+            s_tie = tie_p <= first ? 1.0 : 0.0;
+        }
+    }
+    __syncthreads();
+    const int ps = s_p, kind = s_kind;
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 54);
+    if (ps > hn || kind == 99) return 0;  // no certificate in the head / budget overflow
+    if (kind == 98 || ps < hn) return -1;  // an earlier prefix: its own k-th value is needed
+    if (warp == 0) {
+        double lo = INFINITY, hi = -INFINITY;
+        if (lane < ps) {
+            lo = s_mnq[lane];
+            hi = s_mxq[lane];
+        }
+        if (lane + 32 < ps) {
+            lo = fmin(lo, s_mnq[lane + 32]);
+            hi = fmax(hi, s_mxq[lane + 32]);
+        }
+        lo = warp_min(lo);
+        hi = warp_max(hi);
+        if (lane == 0) {
+            const int n = o.cum[ps];
+            const double lz = __dadd_rn(M, csvd_log(s_zq[ps - 1]));
+            const double lr = o.lrh[ps];
+            const double rho = csvd_rho(lz, lr);
+            const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
+            double xi;
+            if (n < 2 || ps >= D.C) xi = NAN;
+            else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+            double eps_ach = 0.0;
+            if (kind == CSVD_KIND_SOFTMAX_EPS) {
+                eps_ach = rho;
+            } else if (kind == CSVD_KIND_TOPP_MASS) {
+                const double dl = csvd_delta(lz, lr);
+                eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+            }
+            memset(&res, 0, sizeof(res));
+            res.kind = kind;
+            res.fallback = CSVD_FB_NONE;
+            res.sub_size = n;
+            res.clusters_opened = ps;
+            res.heap_pops = ps;
+            res.epsilon_achieved = eps_ach;
+            res.u_max = um;
+            res.topk_min = s_kth;
+            res.rho = rho;
+            res.xi = xi;
+            res.flags = s_tie != 0.0 ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
+        }
+    }
+    __syncthreads();
+    return 1;
+}
+#undef HF_SORT8
+#undef HF_CAS
+
 // The head path; returns true when the step needs the general path (every
 // CTA of the grid / lane returns the same), which the caller then runs from
 // scratch: one call site, so one copy of its code, after the head path's.
@@ -485,6 +723,13 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         __threadfence();
     }
     if (lead) DBG_TS(D, 29);
+    if (D.dbg && tid == 0 && b == 0) {  // debug calibration: 256 dependent f64 adds on this SM
+        double x = D.dbg[58] * 1e-300;
+        const long long c0 = clock64();
+        for (int i = 0; i < 256; ++i) x = __dadd_rn(x, 1e-310);
+        const long long c1 = clock64();
+        D.dbg[57] = (unsigned long long)(c1 - c0) + (x == 12345.0 ? 1 : 0);
+    }
     __shared__ csvd_result s_res;
     bool decided;
     const bool fits = head_fits(D, o, hn) && D.cfg->k <= KH;
@@ -494,13 +739,9 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         D.dbg[62] = o.cum[hn];
     }
     if (fits) {
-        if (D.dbg) {  // debug runs: certify twice, timing the warm repeat (slots 55, 56)
-            head_certify(D, o, hn, hs, s_res);
-            if (lead) DBG_TS(D, 55);
-            head_certify(D, o, hn, hs, s_res);
-            if (lead) DBG_TS(D, 56);
-        }
-        decided = head_certify(D, o, hn, hs, s_res) != 0;
+        const int f = (o.cum[hn] <= 2 * THREADS * 8) ? head_certify_fast(D, o, hn, hs, s_res) : -1;
+        if (lead && D.dbg) D.dbg[59] = (unsigned long long)(f + 2);
+        decided = f < 0 ? head_certify(D, o, hn, hs, s_res) != 0 : f != 0;
     } else {  // a head larger than the h staging area: per-cluster summaries + the sequential scan
         const int k = D.cfg->k;
         double *c_vals = sws, *c_lse = sws + 6 * CHUNK, *c_min = c_lse + CHUNK, *c_max = c_min + CHUNK;

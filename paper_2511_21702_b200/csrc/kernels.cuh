@@ -1719,8 +1719,10 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
             }
             if (lead) DBG_TS(D, 11 + 4 * (st.iter & 3));
         } else {  // MODE_DENSE
+            if (lead) DBG_TS(D, 36);
             dense_rows<ET, CPL, Q>(D, hs_w, scratch);
             grid_sync(D);
+            if (lead) DBG_TS(D, 37);
             if (CTA_ID != 0) {
                 publish_host(D, D.V, nullptr);
                 break;

@@ -49,7 +49,7 @@ def has_gpu() -> bool:
 def golden_names():
     """Small-case fixtures of make_golden.py (full-size ones: make_fullsize.py)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("fullsize_"))
+                  if not os.path.basename(p).startswith(("fullsize_", "harness_")))
 
 
 class GoldenCase:

@@ -13,12 +13,13 @@ from paper_2511_21702_b200 import _lib, workload as wl  # noqa: E402
 V, d, C, g = [int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (128256, 4096, 1024, 16))]
 T = wl.synth_vocab(V, d, C // g, 0.3, 1)
 ix = wl.fast_index(T, C // g, g)
-q = wl.generate_queries(12, d, "contextual", 7, centroids=ix.centroids)
+q = (wl.generate_queries(12, d, "random", 8) if os.environ.get("QUERIES") == "random"
+     else wl.generate_queries(12, d, "contextual", 7, centroids=ix.centroids))
 ctx = P.prepare(T, ix)
 lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
-names = {0: "kernel start", 1: "h staged", 2: "cta0 bounds done", 3: "barrier1 passed",
+names = {36: "dense rows start", 37: "dense rows + barrier done", 0: "kernel start", 1: "h staged", 2: "cta0 bounds done", 3: "barrier1 passed",
          4: "order done (head|full)", 5: "head done", 6: "wave 1 planned", 30: "  U loaded", 31: "  sorted",
          32: "  cum/x done", 33: "  e done", 34: "  lrh done", 35: "  lrh done (RESCALE)",
          40: "  scan: min/max", 41: "  scan: lse prefix", 42: "  scan: 64-merge", 43: "  scan: kth lists",
