@@ -626,6 +626,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemset(L.hcnt, 0, sizeof(int) * (HMAX + 1)));
         CK(cudaMemset(L.bar64, 0, 32));
         L.nblocks = G;
+        L.gsum = nullptr;  // distributed wave summaries: single-step contexts only
         L.dbg = nullptr;
         L.res_host = nullptr;
         L.ids_host = nullptr;
@@ -718,7 +719,9 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemcpy(ctx->d_lanes, td.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_lanes_host, th.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         ctx->kgroup = (getenv("CSVD_LANES_FORKED") || B * G > ctx->grid) ? nullptr : pick_grouped(D0);
-        ctx->kgroup_head = (ctx->kgroup && ctx->kbb) ? pick_head_lanes(D0) : nullptr;
+        // head lanes need row CTAs beside the certifying CTA: with fewer than 4
+        // CTAs per lane (B > 37) the grouped general step spreads the rows better
+        ctx->kgroup_head = (ctx->kgroup && ctx->kbb && G >= 4) ? pick_head_lanes(D0) : nullptr;
         if (ctx->kgroup_head) {
             CK(cudaFuncSetAttribute((const void *)ctx->kgroup_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->smem));
@@ -1109,7 +1112,7 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     if ((rc = dalloc(ctx, &D.res, 1))) return rc;
     if ((rc = dalloc(ctx, &D.bar, 4))) return rc;
     CK(cudaMemset(D.bar, 0, 16));
-    if ((rc = dalloc(ctx, &D.hws, (size_t)HMAX * (3 + KH)))) return rc;
+    if ((rc = dalloc(ctx, &D.gsum, (size_t)D.C * (3 + 32)))) return rc;
     if ((rc = dalloc(ctx, &D.hcnt, (size_t)HMAX + 1))) return rc;
     CK(cudaMemset(D.hcnt, 0, sizeof(int) * (HMAX + 1)));
     if ((rc = dalloc(ctx, &D.bar64, 2))) return rc;

@@ -113,7 +113,7 @@ struct Dev {
     unsigned long long *dbg; // optional phase timestamps (CSVD_DEBUG_TS)
     // head kernel (headstep.cuh): cluster summaries [3*HMAX + HMAX*KH], row /
     // cluster completion counters [HMAX + 1], monotone grid-barrier counter
-    double *hws;
+    double *gsum;  // per-cluster summaries of a wave [3 C + 32 C] (distributed summaries)
     int *hcnt;
     unsigned long long *bar64;
 };
@@ -1013,6 +1013,25 @@ static __device__ double warp_lse_all(const double *vals, int n, double vmax, in
     return __dadd_rn(vmax, csvd_log(s));
 }
 
+// logsumexp over S_logits[0, n) with known max, by the whole CTA (the 64-merge
+// recompute of a chunk, certify.py:79-83: one warp would take ~n / 32 serial exps)
+static __device__ __noinline__ double block_lse_all(const double *vals, int n, double vmax, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double s = 0.0;
+    if (n > 0 && vmax != -INFINITY && vmax != INFINITY)
+        for (int i = threadIdx.x; i < n; i += THREADS) s = __dadd_rn(s, csvd_exp(__dsub_rn(__ldcg(vals + i), vmax)));
+    s = warp_sum(s);
+    __syncthreads();
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (n == 0 || vmax == -INFINITY) return -INFINITY;
+    if (vmax == INFINITY) return INFINITY;
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) t = __dadd_rn(t, red[w]);
+    return __dadd_rn(vmax, csvd_log(t));
+}
+
 struct ScanShared {
     ScanState st;
     csvd_result res;
@@ -1032,7 +1051,7 @@ __device__ __forceinline__ bool near_tie(double x, double thr) {
 static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, ScanShared &ss, int q0, int q1,
                                         const double *c_topk, const double *c_lse, const double *c_min,
                                         const double *c_max, double *c_vals, double *la0, double *lb0,
-                                        double &reg_list, int lane) {
+                                        double &reg_list, int lane, double full_pre = NAN) {
     const ScanState st0 = ss.st;
     const int k = D.cfg->k;
     const bool small_k = k <= 32;
@@ -1080,7 +1099,8 @@ static __device__ __forceinline__ void scan_chunk(const Dev &D, const Ord &o, Sc
     if (rlane < q1 - q0) {
         const double vmax = __shfl_sync(CSVD_FULL, pmx, rlane);
         const int ncum = __shfl_sync(CSVD_FULL, cnt_q, rlane);
-        const double full = warp_lse_all(D.S_logits, ncum, vmax, lane);
+        // the recompute over all of S: precomputed by the whole CTA when given
+        const double full = isnan(full_pre) ? warp_lse_all(D.S_logits, ncum, vmax, lane) : full_pre;
         double rm = (lane > rlane && act) ? lse_q : -INFINITY, rsv = (lane > rlane && act) ? 1.0 : 0.0;
 #pragma unroll 1
         for (int s = 1; s < 32; s <<= 1) {
@@ -1669,10 +1689,35 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
             }
             grid_sync(D);
             if (lead) DBG_TS(D, 9 + 4 * (st.iter & 3));
+            // per-cluster summaries: distributed over the grid (each cluster
+            // summarised once, into D.gsum, then one grid barrier) when the
+            // wave is wider than one CTA's warps; else redundantly per CTA
+            const bool dist = D.gsum && k <= 32 && D.lanes == nullptr && st.p_hi - st.p_lo > WARPS;
+            const double *g_lse = D.gsum, *g_min = D.gsum + D.C, *g_max = D.gsum + 2 * D.C;
+            const double *g_topk = D.gsum + 3 * D.C;  // [C][32]
+            if (dist) {
+#pragma unroll 1
+                for (int q = st.p_lo + CTA_ID * WARPS + warp; q < st.p_hi; q += CTA_N * WARPS) {
+                    double pre[SUM_E];
+                    summary_load(D, o.cum[q], o.cum[q + 1], pre, lane);
+                    cluster_summary(D, o.cum[q], o.cum[q + 1], k, D.gsum + 3 * D.C + (size_t)q * 32, D.gsum + q,
+                                    D.gsum + D.C + q, D.gsum + 2 * D.C + q, pre, lane);
+                }
+                if (lane == 0) __threadfence();
+                grid_sync(D);
+            }
             // summaries + scan, chunk by chunk (identical in every CTA)
             for (int q0 = st.p_lo; q0 < st.p_hi; q0 += D.chunk) {
                 const int q1 = min(st.p_hi, q0 + D.chunk);
-                {  // the loads of this warp's next two clusters are always in flight
+                if (dist) {
+                    for (int i = threadIdx.x; i < q1 - q0; i += THREADS) {
+                        c_lse[i] = __ldcg(g_lse + q0 + i);
+                        c_min[i] = __ldcg(g_min + q0 + i);
+                        c_max[i] = __ldcg(g_max + q0 + i);
+                    }
+                    for (int i = threadIdx.x; i < (q1 - q0) * k; i += THREADS)
+                        c_topk[i] = __ldcg(g_topk + (size_t)(q0 + i / k) * 32 + i % k);
+                } else {  // the loads of this warp's next two clusters are always in flight
                     double pre[2][SUM_E];
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
@@ -1691,7 +1736,19 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
                 }
                 __syncthreads();
                 if (lead) DBG_TS(D, 10 + 4 * (st.iter & 3));
-                if (warp == 0) scan_chunk(D, o, ss, q0, q1, c_topk, c_lse, c_min, c_max, c_vals, la, lb, reg_list, lane);
+                double full_pre = NAN;
+                {  // this chunk's 64-merge recompute (certify.py:79-83), by the whole CTA
+                    const int rl = (q0 / 64) * 64 + 63 - q0;
+                    if (rl < q1 - q0) {
+                        __shared__ double s_red2[WARPS];
+                        double vmax = ss.st.p > 0 ? ss.st.smax : -INFINITY;
+                        for (int t = 0; t <= rl; ++t) vmax = fmax(vmax, c_max[t]);
+                        full_pre = block_lse_all(D.S_logits, o.cum[q0 + rl + 1], vmax, s_red2);
+                    }
+                }
+                if (warp == 0)
+                    scan_chunk(D, o, ss, q0, q1, c_topk, c_lse, c_min, c_max, c_vals, la, lb, reg_list, lane,
+                               full_pre);
                 __syncthreads();
                 if (ss.st.phase != PH_MAIN && ss.st.phase != PH_PE) break;
             }
@@ -1809,40 +1866,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int qb = 0; qb < B; qb += gq) {
         const int nq = min(gq, B - qb);
         tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / gq));
-        if (D.C <= nwarps && gq > BQN) {
-            // one cluster per warp: the registers a second row would take hold
-            // more queries instead, so fewer passes re-read the centroids
-            const int c = gwarp;
-            if (c < D.C) {
-                const double *const rows[1] = {D.cent + (size_t)c * D.bd};
-                double dots[1][BQN1];
-                warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
-                if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
+        // one cluster per warp task (looping over the clusters), the
+        // registers a second row would take hold more queries instead; the
+        // row's next element step is in flight while the current one is used
+#pragma unroll 1
+        for (int c = gwarp; c < D.C; c += nwarps) {
+            const double *const rows[1] = {D.cent + (size_t)c * D.bd};
+            double dots[1][BQN1];
+            warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
+            if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
 #pragma unroll
-                    for (int j = 0; j < BQN1; ++j)
-                        if (j < nq) dots_l[qb + j][c] = dots[0][j];
-                }
-            }
-        } else {
-            // two clusters per warp at a time: each staged query value read
-            // from shared memory feeds both rows
-            for (int j0 = 0; j0 < nq; j0 += BQN) {
-                const int nq2 = min(BQN, nq - j0);
-                for (int c = gwarp; c < D.C; c += 2 * nwarps) {
-                    const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
-                    const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
-                    double dots[2][BQN];
-                    warp_dot_regular_multi<BQ, BQN, 2>(rows, smem + (size_t)j0 * hs_stride, hs_stride, nq2,
-                                                       D.bplan.leaf_len, lane, dots);
-                    if (lane == 0) {
-#pragma unroll
-                        for (int j = 0; j < BQN; ++j)
-                            if (j < nq2) {
-                                dots_l[qb + j0 + j][c] = dots[0][j];
-                                if (c2 != c) dots_l[qb + j0 + j][c2] = dots[1][j];
-                            }
-                    }
-                }
+                for (int j = 0; j < BQN1; ++j)
+                    if (j < nq) dots_l[qb + j][c] = dots[0][j];
             }
         }
         __syncthreads();

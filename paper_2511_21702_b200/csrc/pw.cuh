@@ -316,7 +316,6 @@ template <int Q, int NQ, int NR>
 __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&rows)[NR],
                                                        const double *__restrict__ hs0, int hs_stride, int nq,
                                                        int leaf_len, int lane, double (&out)[NR][NQ]) {
-    constexpr int NB = 2;
     const int S = leaf_len >> 3;
     // slice totals combined as they complete, in the (s0+s1)+(s2+s3) tree of
     // warp_dot_regular: at most two partials per (row, query) stay live
@@ -325,45 +324,45 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&row
     for (int u = 0; u < Q; ++u) {
         const double *hp = hs0 + (size_t)(u * 32 + lane) * (leaf_len + 2);
         double r[NR][NQ][8];
-#pragma unroll
-        for (int w = 0; w < NR; ++w)
-#pragma unroll
-            for (int j = 0; j < NQ; ++j)
-#pragma unroll
-                for (int c = 0; c < 8; ++c) r[w][j][c] = 0.0;
-        for (int i0 = 0; i0 < S; i0 += NB) {
-            Raw<double, 8> raw[NR][NB];
+        // one element step of every row per buffer, the next step's loads in
+        // flight while the current one is multiplied into every query
+        Raw<double, 8> A[NR], B[NR];
+        auto load = [&](Raw<double, 8>(&buf)[NR], int i) {
 #pragma unroll
             for (int w = 0; w < NR; ++w)
+                if (i < S) buf[w].load(rows[w] + (size_t)(u * 32 + lane) * leaf_len + i * 8);
+        };
+        auto consume = [&](const Raw<double, 8>(&buf)[NR], int i) {
+            if (i < S) {
 #pragma unroll
-                for (int s = 0; s < NB; ++s)
-                    if (i0 + s < S) raw[w][s].load(rows[w] + (size_t)(u * 32 + lane) * leaf_len + (i0 + s) * 8);
+                for (int j = 0; j < NQ; ++j) {
+                    if (j < nq) {
+                        const double2 *h2 = reinterpret_cast<const double2 *>(hp + (size_t)j * hs_stride + 8 * i);
+                        double hv[8];
 #pragma unroll
-            for (int s = 0; s < NB; ++s) {
-                if (i0 + s < S) {
-                    const int i = i0 + s;
-#pragma unroll
-                    for (int j = 0; j < NQ; ++j) {
-                        if (j < nq) {
-                            const double2 *h2 = reinterpret_cast<const double2 *>(hp + (size_t)j * hs_stride + 8 * i);
-                            double hv[8];
-#pragma unroll
-                            for (int c2 = 0; c2 < 4; ++c2) {
-                                const double2 t = h2[c2];
-                                hv[2 * c2] = t.x;
-                                hv[2 * c2 + 1] = t.y;
-                            }
-#pragma unroll
-                            for (int w = 0; w < NR; ++w)
-#pragma unroll
-                                for (int c = 0; c < 8; ++c) {
-                                    const double pr = d_mul(raw[w][s].get(c), hv[c]);
-                                    r[w][j][c] = (i == 0) ? pr : d_add(r[w][j][c], pr);
-                                }
+                        for (int c2 = 0; c2 < 4; ++c2) {
+                            const double2 t = h2[c2];
+                            hv[2 * c2] = t.x;
+                            hv[2 * c2 + 1] = t.y;
                         }
+#pragma unroll
+                        for (int w = 0; w < NR; ++w)
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                const double pr = d_mul(buf[w].get(c), hv[c]);
+                                r[w][j][c] = (i == 0) ? pr : d_add(r[w][j][c], pr);
+                            }
                     }
                 }
             }
+        };
+        load(A, 0);
+#pragma unroll 1
+        for (int i = 0; i < S; i += 2) {
+            load(B, i + 1);
+            consume(A, i);
+            load(A, i + 2);
+            consume(B, i + 1);
         }
 #pragma unroll
         for (int w = 0; w < NR; ++w)
