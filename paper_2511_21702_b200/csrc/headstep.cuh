@@ -639,8 +639,8 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         // ---- rows of the head, contiguous per row CTA
         const int rb = solo ? 0 : b - 1, Gr = solo ? 1 : G - 1;
         const int r_lo = (int)((long long)R * rb / Gr), r_hi = (int)((long long)R * (rb + 1) / Gr);
-#pragma unroll 1
-        for (int r = r_lo + warp; r < r_hi; r += WARPS) {
+        // two rows per warp at a time (r, r + WARPS): both in flight, h read once
+        auto locate = [&](int r, int &wrow, int &pos) {
             int lo = 0, hi = hn;  // cum[lo] <= r < cum[lo+1]
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
@@ -648,11 +648,29 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             }
             const int c = o.order[lo];
             const int i = r - o.cum[lo];
-            const int pos = __ldg(D.starts + c) + i;
-            const double logit = row_logit<ET, 8, Q>(D, __ldg(D.wrow0 + c) + i, pos, hs, nullptr, lane);
+            pos = __ldg(D.starts + c) + i;
+            wrow = __ldg(D.wrow0 + c) + i;
+        };
+        const ET *Wt = reinterpret_cast<const ET *>(D.W);
+#pragma unroll 1
+        for (int r = r_lo + warp; r < r_hi; r += 2 * WARPS) {
+            const int r2 = r + WARPS;
+            int wa, pa, wb, pb;
+            locate(r, wa, pa);
+            if (r2 < r_hi) locate(r2, wb, pb);
+            else {
+                wb = wa;
+                pb = pa;
+            }
+            double la, lb;
+            warp_dot_r8_x2<ET, Q>(Wt + (size_t)wa * D.d, Wt + (size_t)wb * D.d, hs, D.wplan.leaf_len, lane, la, lb);
             if (lane == 0) {
-                D.S_logits[r] = logit;
-                D.S_ids[r] = __ldg(D.perm + pos);
+                D.S_logits[r] = __dadd_rn(la, __ldg(D.bias + pa));
+                D.S_ids[r] = __ldg(D.perm + pa);
+                if (r2 < r_hi) {
+                    D.S_logits[r2] = __dadd_rn(lb, __ldg(D.bias + pb));
+                    D.S_ids[r2] = __ldg(D.perm + pb);
+                }
             }
         }
         if (lane == 0) __threadfence();

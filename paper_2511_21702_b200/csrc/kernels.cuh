@@ -1297,11 +1297,7 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
             const int r = gwarp + j * nwarps;
             if (r < D.Vl) bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)r * rb, rb);
         }
-    for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
-        const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
-        if (PD > 0 && lane == 0 && lr + PD * nwarps < D.Vl)
-            bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(lr + PD * nwarps) * rb, rb);
-        const double logit = row_logit<ET, CPL, Q>(D, lr, pos, hs, scratch, lane);
+    auto take = [&](int pos, double logit) {
         if (lane == 0) {
             const int tok = __ldg(D.perm + pos);
             D.S_logits[tok] = logit;
@@ -1320,6 +1316,26 @@ __device__ void dense_rows(const Dev &D, const double *hs, double *scratch) {
             mylist[i] = logit;
             if (cnt < k) cnt++;
             kmin = mylist[cnt - 1];
+        }
+    };
+    if constexpr (CPL == 8) {  // two rows per warp at a time: both in flight, h read once
+        const ET *Wt = reinterpret_cast<const ET *>(D.W);
+#pragma unroll 1
+        for (int lr = gwarp; lr < D.Vl; lr += 2 * nwarps) {
+            const int lr2 = lr + nwarps < D.Vl ? lr + nwarps : lr;
+            const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
+            const int pos2 = D.lpos ? __ldg(D.lpos + lr2) : lr2;
+            double la, lb;
+            warp_dot_r8_x2<ET, Q>(Wt + (size_t)lr * D.d, Wt + (size_t)lr2 * D.d, hs, D.wplan.leaf_len, lane, la, lb);
+            take(pos, __dadd_rn(la, __ldg(D.bias + pos)));
+            if (lr2 != lr) take(pos2, __dadd_rn(lb, __ldg(D.bias + pos2)));
+        }
+    } else {
+        for (int lr = gwarp; lr < D.Vl; lr += nwarps) {
+            const int pos = D.lpos ? __ldg(D.lpos + lr) : lr;
+            if (PD > 0 && lane == 0 && lr + PD * nwarps < D.Vl)
+                bulk_prefetch_l2(reinterpret_cast<const char *>(D.W) + (size_t)(lr + PD * nwarps) * rb, rb);
+            take(pos, row_logit<ET, CPL, Q>(D, lr, pos, hs, scratch, lane));
         }
     }
     if (small_k) {

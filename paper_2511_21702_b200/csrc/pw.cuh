@@ -231,6 +231,92 @@ __device__ __forceinline__ double warp_dot_r8(const ET *__restrict__ row, const 
     return d_add(0.0, tot);
 }
 
+// Two rows per warp (CPL = 8): both rows' leaf loads in flight together and
+// every staged h value read once for both (half the shared-memory reads of
+// two single-row dots).  Same tree as warp_dot_r8 for each row.
+template <typename ET, int Q>
+__device__ __forceinline__ void warp_dot_r8_x2(const ET *__restrict__ rowA, const ET *__restrict__ rowB,
+                                               const double *__restrict__ hs, int leaf_len, int lane, double &outA,
+                                               double &outB) {
+    constexpr int NB = NBatch<ET, 8>::value / 4;  // loads per row per buffer
+    const int S = leaf_len >> 3;
+    double slA[Q], slB[Q];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+        const ET *la = rowA + (size_t)(u * 32 + lane) * leaf_len;
+        const ET *lb = rowB + (size_t)(u * 32 + lane) * leaf_len;
+        const double *hp = hs + (size_t)(u * 32 + lane) * (leaf_len + 2);
+        double ra[8], rb[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            ra[c] = 0.0;
+            rb[c] = 0.0;
+        }
+        Raw<ET, 8> A0[NB], A1[NB], B0[NB], B1[NB];
+        auto load = [&](Raw<ET, 8>(&xa)[NB], Raw<ET, 8>(&xb)[NB], int i0) {
+#pragma unroll
+            for (int s = 0; s < NB; ++s)
+                if (i0 + s < S) {
+                    xa[s].load(la + (i0 + s) * 8);
+                    xb[s].load(lb + (i0 + s) * 8);
+                }
+        };
+        auto consume = [&](const Raw<ET, 8>(&xa)[NB], const Raw<ET, 8>(&xb)[NB], int i0) {
+#pragma unroll
+            for (int s = 0; s < NB; ++s) {
+                const int i = i0 + s;
+                if (i < S) {
+                    const double2 *h2 = reinterpret_cast<const double2 *>(hp + 8 * i);
+                    double hv[8];
+#pragma unroll
+                    for (int c2 = 0; c2 < 4; ++c2) {
+                        const double2 t = h2[c2];
+                        hv[2 * c2] = t.x;
+                        hv[2 * c2 + 1] = t.y;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double pa = d_mul(xa[s].get(c), hv[c]);
+                        const double pb = d_mul(xb[s].get(c), hv[c]);
+                        ra[c] = (i == 0) ? pa : d_add(ra[c], pa);
+                        rb[c] = (i == 0) ? pb : d_add(rb[c], pb);
+                    }
+                }
+            }
+        };
+        load(A0, B0, 0);
+#pragma unroll 1
+        for (int i0 = 0; i0 < S; i0 += 2 * NB) {
+            load(A1, B1, i0 + NB);
+            consume(A0, B0, i0);
+            load(A0, B0, i0 + 2 * NB);
+            consume(A1, B1, i0 + NB);
+        }
+        double va = d_add(d_add(d_add(ra[0], ra[1]), d_add(ra[2], ra[3])), d_add(d_add(ra[4], ra[5]), d_add(ra[6], ra[7])));
+        double vb = d_add(d_add(d_add(rb[0], rb[1]), d_add(rb[2], rb[3])), d_add(d_add(rb[4], rb[5]), d_add(rb[6], rb[7])));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            va = d_add(va, __shfl_xor_sync(CSVD_FULL, va, o));
+            vb = d_add(vb, __shfl_xor_sync(CSVD_FULL, vb, o));
+        }
+        slA[u] = va;
+        slB[u] = vb;
+    }
+    double ta, tb;
+    if constexpr (Q == 1) {
+        ta = slA[0];
+        tb = slB[0];
+    } else if constexpr (Q == 2) {
+        ta = d_add(slA[0], slA[1]);
+        tb = d_add(slB[0], slB[1]);
+    } else {
+        ta = d_add(d_add(slA[0], slA[1]), d_add(slA[2], slA[3]));
+        tb = d_add(d_add(slB[0], slB[1]), d_add(slB[2], slB[3]));
+    }
+    outA = d_add(0.0, ta);
+    outB = d_add(0.0, tb);
+}
+
 template <typename ET, int CPL, int Q>
 __device__ __forceinline__ double warp_dot_regular(const ET *__restrict__ row,
                                                    const double *__restrict__ hs,
