@@ -620,7 +620,7 @@ def run_ours(a):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
                      "traffic": traffic, "peak_kind": pk_kind,
-                     "kernel": "k_step (one persistent cooperative launch per step; bounds, head, rows, certification)",
+                     "kernel": "k_head (one cooperative launch per step: bounds, head order, rows, certification; the general step in the same launch when undecided)",
                      "algorithmic_bytes_per_step": mean_bytes},
         "fallback_rate": fallbacks / K,
         "mean_sub_ratio": float(np.mean([o.stats.ratio for o in outs])),

@@ -584,10 +584,14 @@ static int lalloc(csvd_ctx *ctx, T **p, size_t count) {
     return 0;
 }
 
-// B lanes, each a full per-step workspace and a grid of max(1, grid / B) CTAs
+#define LANE_MIN_G 1  // CTAs per batch lane at least (4 measured no better for c4 / c5: the
+                      // lanes' rows are not the large-batch bottleneck)
+// B lanes, each a full per-step workspace and a grid of max(LANE_MIN_G, grid / B) CTAs
 static int ensure_lanes(csvd_ctx *ctx, int B) {
     const Dev &D0 = ctx->D;
-    const int G = ctx->grid / B > 0 ? ctx->grid / B : 1;
+    // CTAs per lane: the grid split B ways, but at least LANE_MIN_G (large
+    // batches then run in sub-batches of grid / G lanes, one launch each)
+    const int G = std::min(ctx->grid, std::max(ctx->grid / B, std::min(LANE_MIN_G, ctx->grid)));
     if ((int)ctx->lanes.size() == B && ctx->lane_grid == G && ctx->lane_K == D0.K) return 0;
     free_lanes(ctx);
     const int C = D0.C, V = D0.V, K = D0.K;
@@ -718,23 +722,24 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         if ((rc = lalloc(ctx, &ctx->d_lanes, B)) || (rc = lalloc(ctx, &ctx->d_lanes_host, B))) return rc;
         CK(cudaMemcpy(ctx->d_lanes, td.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_lanes_host, th.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
-        ctx->kgroup = (getenv("CSVD_LANES_FORKED") || B * G > ctx->grid) ? nullptr : pick_grouped(D0);
+        const int LB = std::min(B, ctx->grid / G);  // lanes per launch
+        ctx->kgroup = getenv("CSVD_LANES_FORKED") ? nullptr : pick_grouped(D0);
         // head lanes need row CTAs beside the certifying CTA: with fewer than 4
         // CTAs per lane (B > 37) the grouped general step spreads the rows better
-        ctx->kgroup_head = (ctx->kgroup && ctx->kbb && G >= 4) ? pick_head_lanes(D0) : nullptr;
+        ctx->kgroup_head = (ctx->kgroup && ctx->kbb && G >= LANE_MIN_G) ? pick_head_lanes(D0) : nullptr;
         if (ctx->kgroup_head) {
             CK(cudaFuncSetAttribute((const void *)ctx->kgroup_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->smem));
             int occ = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kgroup_head, THREADS, ctx->smem));
-            if (occ * ctx->nsm < B * G) ctx->kgroup_head = nullptr;
+            if (occ * ctx->nsm < LB * G) ctx->kgroup_head = nullptr;
         }
         if (ctx->kgroup) {
             CK(cudaFuncSetAttribute((const void *)ctx->kgroup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->smem));
             int occ = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->kgroup, THREADS, ctx->smem));
-            if (occ * ctx->nsm < B * G) ctx->kgroup = nullptr;
+            if (occ * ctx->nsm < LB * G) ctx->kgroup = nullptr;
         }
     }
     ctx->lane_grid = G;
@@ -766,10 +771,16 @@ static int capture_batch(csvd_ctx *ctx, int B, bool host_io, bool head) {
         Dev Dg = host_io ? ctx->lanes[0].Dh : ctx->lanes[0].D;
         Dg.launch_mode = LAUNCH_STEP;
         Dg.lanes = host_io ? ctx->d_lanes_host : ctx->d_lanes;
-        void *args[] = {&Dg};
         const kern_t kl = (head && ctx->kgroup_head) ? ctx->kgroup_head : ctx->kgroup;
-        CK(cudaLaunchCooperativeKernel((const void *)kl, dim3(B * ctx->lane_grid), dim3(THREADS), args,
-                                       ctx->smem, s));
+        const LaneWS *base = Dg.lanes;
+        const int LB = ctx->grid / ctx->lane_grid;  // lanes per launch (sub-batches for large B)
+        for (int first = 0; first < B; first += LB) {
+            const int n = std::min(LB, B - first);
+            Dg.lanes = base + first;
+            void *args[] = {&Dg};
+            CK(cudaLaunchCooperativeKernel((const void *)kl, dim3(n * ctx->lane_grid), dim3(THREADS), args,
+                                           ctx->smem, s));
+        }
         CK(cudaStreamEndCapture(s, &g));
         CK(cudaGraphInstantiate(&ctx->g_batch, g, 0));
         CK(cudaGraphDestroy(g));
@@ -834,7 +845,9 @@ extern "C" int csvd_step_batch_device(csvd_ctx *ctx, int32_t B, const double *H_
     if (H_dev != ctx->d_H)
         CK(cudaMemcpyAsync(ctx->d_H, H_dev, sizeof(double) * B * ctx->D.d, cudaMemcpyDeviceToDevice, s));
     CK(cudaGraphLaunch(ctx->g_batch, s));
-    ctx->last_launches = (ctx->kbb ? 1 : 0) + (ctx->kgroup ? 1 : ctx->g_batch_B);
+    ctx->last_launches = (ctx->kbb ? 1 : 0) +
+                         (ctx->kgroup ? (ctx->g_batch_B + ctx->grid / ctx->lane_grid - 1) / (ctx->grid / ctx->lane_grid)
+                                      : ctx->g_batch_B);
     return 0;
 }
 
@@ -852,7 +865,9 @@ extern "C" int csvd_step_batch_host(csvd_ctx *ctx, int32_t B, const double *H, c
     for (int b = 0; b < B; ++b) ctx->res_map_b[b].kind = CSVD_KIND_NONE - 1;  // sentinels, overwritten by the lanes
     auto t1 = now();
     CK(cudaGraphLaunch(ctx->g_batch, s));
-    ctx->last_launches = (ctx->kbb ? 1 : 0) + (ctx->kgroup ? 1 : ctx->g_batch_B);
+    ctx->last_launches = (ctx->kbb ? 1 : 0) +
+                         (ctx->kgroup ? (ctx->g_batch_B + ctx->grid / ctx->lane_grid - 1) / (ctx->grid / ctx->lane_grid)
+                                      : ctx->g_batch_B);
     auto t2 = now();
     // every lane publishes its result into mapped memory; busy-poll the stream
     cudaError_t q;

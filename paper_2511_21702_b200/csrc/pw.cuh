@@ -410,45 +410,52 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&row
     for (int u = 0; u < Q; ++u) {
         const double *hp = hs0 + (size_t)(u * 32 + lane) * (leaf_len + 2);
         double r[NR][NQ][8];
-        // one element step of every row per buffer, the next step's loads in
-        // flight while the current one is multiplied into every query
-        Raw<double, 8> A[NR], B[NR];
-        auto load = [&](Raw<double, 8>(&buf)[NR], int i) {
+        // MB element steps of every row per buffer, the next buffer's loads
+        // in flight while the current one is multiplied into every query
+        constexpr int MB = 2;
+        Raw<double, 8> A[MB][NR], B[MB][NR];
+        auto load = [&](Raw<double, 8>(&buf)[MB][NR], int i0) {
 #pragma unroll
-            for (int w = 0; w < NR; ++w)
-                if (i < S) buf[w].load(rows[w] + (size_t)(u * 32 + lane) * leaf_len + i * 8);
+            for (int m = 0; m < MB; ++m)
+#pragma unroll
+                for (int w = 0; w < NR; ++w)
+                    if (i0 + m < S) buf[m][w].load(rows[w] + (size_t)(u * 32 + lane) * leaf_len + (i0 + m) * 8);
         };
-        auto consume = [&](const Raw<double, 8>(&buf)[NR], int i) {
-            if (i < S) {
+        auto consume = [&](const Raw<double, 8>(&buf)[MB][NR], int i0) {
 #pragma unroll
-                for (int j = 0; j < NQ; ++j) {
-                    if (j < nq) {
-                        const double2 *h2 = reinterpret_cast<const double2 *>(hp + (size_t)j * hs_stride + 8 * i);
-                        double hv[8];
+            for (int m = 0; m < MB; ++m) {
+                const int i = i0 + m;
+                if (i < S) {
 #pragma unroll
-                        for (int c2 = 0; c2 < 4; ++c2) {
-                            const double2 t = h2[c2];
-                            hv[2 * c2] = t.x;
-                            hv[2 * c2 + 1] = t.y;
-                        }
+                    for (int j = 0; j < NQ; ++j) {
+                        if (j < nq) {
+                            const double2 *h2 = reinterpret_cast<const double2 *>(hp + (size_t)j * hs_stride + 8 * i);
+                            double hv[8];
 #pragma unroll
-                        for (int w = 0; w < NR; ++w)
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) {
-                                const double pr = d_mul(buf[w].get(c), hv[c]);
-                                r[w][j][c] = (i == 0) ? pr : d_add(r[w][j][c], pr);
+                            for (int c2 = 0; c2 < 4; ++c2) {
+                                const double2 t = h2[c2];
+                                hv[2 * c2] = t.x;
+                                hv[2 * c2 + 1] = t.y;
                             }
+#pragma unroll
+                            for (int w = 0; w < NR; ++w)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) {
+                                    const double pr = d_mul(buf[m][w].get(c), hv[c]);
+                                    r[w][j][c] = (i == 0) ? pr : d_add(r[w][j][c], pr);
+                                }
+                        }
                     }
                 }
             }
         };
         load(A, 0);
 #pragma unroll 1
-        for (int i = 0; i < S; i += 2) {
-            load(B, i + 1);
+        for (int i = 0; i < S; i += 2 * MB) {
+            load(B, i + MB);
             consume(A, i);
-            load(A, i + 2);
-            consume(B, i + 1);
+            load(A, i + 2 * MB);
+            consume(B, i + MB);
         }
 #pragma unroll
         for (int w = 0; w < NR; ++w)
