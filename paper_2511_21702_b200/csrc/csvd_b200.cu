@@ -724,9 +724,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemcpy(ctx->d_lanes_host, th.data(), sizeof(LaneWS) * B, cudaMemcpyHostToDevice));
         const int LB = std::min(B, ctx->grid / G);  // lanes per launch
         ctx->kgroup = getenv("CSVD_LANES_FORKED") ? nullptr : pick_grouped(D0);
-        // head lanes need row CTAs beside the certifying CTA: with fewer than 4
-        // CTAs per lane (B > 37) the grouped general step spreads the rows better
-        ctx->kgroup_head = (ctx->kgroup && ctx->kbb && G >= LANE_MIN_G) ? pick_head_lanes(D0) : nullptr;
+        ctx->kgroup_head = (ctx->kgroup && ctx->kbb) ? pick_head_lanes(D0) : nullptr;
         if (ctx->kgroup_head) {
             CK(cudaFuncSetAttribute((const void *)ctx->kgroup_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)ctx->smem));

@@ -634,10 +634,11 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     const unsigned long long epoch = s_epoch;
     unsigned long long *decision = D.bar64 + 1;  // epoch * 2 + decided
     const int R = o.cum[hn];
-    const bool solo = G == 1;  // a one-CTA lane computes its rows itself
-    if (b > 0 || solo) {
+    // small lanes (G <= 3 CTAs): CTA 0 computes rows too, then certifies
+    const bool cta0_rows = G <= 3;
+    if (b > 0 || cta0_rows) {
         // ---- rows of the head, contiguous per row CTA
-        const int rb = solo ? 0 : b - 1, Gr = solo ? 1 : G - 1;
+        const int rb = cta0_rows ? b : b - 1, Gr = cta0_rows ? G : G - 1;
         const int r_lo = (int)((long long)R * rb / Gr), r_hi = (int)((long long)R * (rb + 1) / Gr);
         // two rows per warp at a time (r, r + WARPS): both in flight, h read once
         auto locate = [&](int r, int &wrow, int &pos) {
@@ -683,9 +684,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                 D.ids_host[r] = __ldcg(D.S_ids + r);
             }
         }
-        if (!solo) {
-            // this CTA's share of every cluster it touches, then its arrival
-            // (release: the rows above are visible first)
+        if (G > 1) {  // this CTA's share of every cluster it touches (release: rows visible first)
             if (tid < hn) {
                 const int a = max(o.cum[tid], r_lo), e = min(o.cum[tid + 1], r_hi);
                 if (e > a) {
@@ -694,6 +693,8 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                 }
             }
             __syncthreads();
+        }
+        if (b > 0) {  // then its arrival, and CTA 0's decision
             if (tid == 0) {
                 __threadfence();
                 atomicAdd(D.hcnt + HMAX, 1);
@@ -723,7 +724,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         }
     }
     // ---- CTA 0: wait for every head cluster's rows and every row CTA, then certify
-    if (!solo) {
+    if (G > 1) {
         for (int q = tid; q <= hn; q += THREADS) {
             const int n = q < hn ? o.cum[q + 1] - o.cum[q] : G - 1;
             const int *ctr = D.hcnt + (q < hn ? q : HMAX);
