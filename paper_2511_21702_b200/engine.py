@@ -154,6 +154,7 @@ class DeviceIndex:
                 except ValueError:
                     pass
         self._cfg_cache = {}
+        self._cfg_last = None
         self._lock = threading.Lock()
         self._res = _lib.Result()
         self._ids = np.empty(self.V, dtype=np.int64)
@@ -186,6 +187,9 @@ class DeviceIndex:
                     first_wave_tokens: int = 0) -> _lib.Config:
         """csvd_config for `cfg`; memoized per (frozen, hashable) config since
         validating and flattening it costs more host time than the launch."""
+        last = self._cfg_last  # the same config object as the previous step: no hashing
+        if last is not None and last[0] is cfg and last[1] == (k_max, variant, first_wave_tokens):
+            return last[2]
         try:
             key = (cfg, k_max, variant, first_wave_tokens)
             hit = self._cfg_cache.get(key)
@@ -196,6 +200,8 @@ class DeviceIndex:
             if len(self._cfg_cache) > 256:
                 self._cfg_cache.clear()
             self._cfg_cache[key] = hit
+        if getattr(cfg, "__dataclass_params__", None) is not None and cfg.__dataclass_params__.frozen:
+            self._cfg_last = (cfg, (k_max, variant, first_wave_tokens), hit)  # immutable: safe to key by identity
         return hit
 
     # --- step -------------------------------------------------------------
@@ -350,14 +356,22 @@ def _cache_get(key, objs, factory):
         return ctx
 
 
+_LAST = [None, None, None, None]  # table, index, device, context of the last prepare()
+
+
 def prepare(table, index, device: int | None = None) -> DeviceIndex:
     """Upload (table, index) once; later steps on the same objects reuse it."""
     dev = DEFAULT_DEVICE if device is None else device
-    return _cache_get(("ti", id(table), id(index), dev), (table, index),
-                      lambda: DeviceIndex(table, index, dev))
+    last = _LAST  # weak: the last pair must not outlive its owner
+    if last[0] is not None and last[0]() is table and last[1]() is index and last[2] == dev and last[3]._ctx:
+        return last[3]  # the common decode loop: the same pair every step
+    ctx = _cache_get(("ti", id(table), id(index), dev), (table, index), lambda: DeviceIndex(table, index, dev))
+    _LAST[:] = [weakref.ref(table), weakref.ref(index), dev, ctx]
+    return ctx
 
 
 def clear_cache():
+    _LAST[:] = [None, None, None, None]
     with _CACHE_LOCK:
         for _, ctx in _CACHE.values():
             ctx.close()
