@@ -412,7 +412,7 @@ __device__ __forceinline__ void warp_dot_regular_multi(const double *const (&row
         double r[NR][NQ][8];
         // MB element steps of every row per buffer, the next buffer's loads
         // in flight while the current one is multiplied into every query
-        constexpr int MB = 2;
+        constexpr int MB = NR == 1 ? 2 : 1;  // register budget: 2 steps for one row, 1 for two
         Raw<double, 8> A[MB][NR], B[MB][NR];
         auto load = [&](Raw<double, 8>(&buf)[MB][NR], int i0) {
 #pragma unroll

@@ -201,3 +201,21 @@ def test_refined_bias_bound_matches_oracle_and_reference_rules(mode):
             assert close(P.refined_bias_bound(ix, c, h, tabled, bias=T.bias), geom + rest, tol)
             assert close(P.refined_bias_bound(ix, c, h, tabled), geom + meta.bias_topm[-1][0], tol)
         assert P.refined_bias_bound(ix, c, h, set(members)) == float("-inf")
+
+
+def test_tie_ambiguous_flag():
+    """A softmax decision exactly at its threshold (eps = the reference's rho at
+    the certifying prefix) is flagged as an ulp-level tie; a clear margin is not."""
+    import paper_2511_21702_b200 as P
+    from paper_2511_21702_b200 import workload as wl
+    T = wl.synth_vocab(20000, 512, 40, 0.3, 1)
+    ix = wl.fast_index(T, 40, 4)
+    h = wl.generate_queries(1, 512, "contextual", 7, centroids=ix.centroids)[0]
+    base = P.DecodeConfig(k=10, epsilon=0.05, targets=("softmax_eps",))
+    exp = O.decode_step(T, ix, h, base)
+    assert exp.status.kind == "softmax_eps"
+    out = P.decode_step(T, ix, h, base)
+    assert not out.stats.tie_ambiguous
+    tie = P.DecodeConfig(k=10, epsilon=float(exp.stats["rho"]), targets=("softmax_eps",))
+    out = P.decode_step(T, ix, h, tie)
+    assert out.stats.tie_ambiguous
