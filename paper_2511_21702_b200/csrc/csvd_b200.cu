@@ -80,6 +80,8 @@ struct csvd_ctx {
     csvd_config *d_cfg = nullptr;
     double *d_h = nullptr;
     double *h_pin = nullptr;
+    double *h_map = nullptr;  // mapped pinned query: the host-API head graph reads it in place (zero-copy)
+    bool h_zero_copy = false;
     // pinned staging configs, one per kind of graph that reads one at execution
     // time (step/shard: cfg_pin; batch: cfg_pin_b; dense/bounds: cfg_pin_fixed)
     csvd_config *cfg_pin = nullptr, *cfg_pin_b = nullptr, *cfg_pin_fixed = nullptr;
@@ -496,8 +498,14 @@ static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
     cudaStream_t s = ctx->stream;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    if (host_io) CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
     Dev D = host_io ? ctx->Dhost : ctx->D;
+    if (host_io && ctx->h_zero_copy) {  // the kernel stages h straight from mapped host memory
+        void *p = nullptr;
+        CK(cudaHostGetDevicePointer(&p, ctx->h_map, 0));
+        D.h = (const double *)p;
+    } else if (host_io) {
+        CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * ctx->D.d, cudaMemcpyHostToDevice, s));
+    }
     D.launch_mode = LAUNCH_STEP;
     void *args[] = {&D};
     cudaError_t e = cudaLaunchCooperativeKernel((const void *)ctx->khead, dim3(ctx->grid), dim3(THREADS), args,
@@ -1143,6 +1151,8 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     // --- pinned staging
     ctx->first_chunk = D.V < 4096 ? D.V : 4096;
     CK(cudaHostAlloc(&ctx->h_pin, sizeof(double) * (D.d + 1), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->h_map, sizeof(double) * (D.d + 1), cudaHostAllocMapped));
+    ctx->h_zero_copy = getenv("CSVD_H_COPY") == nullptr;
     CK(cudaHostAlloc(&ctx->cfg_pin, sizeof(csvd_config), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->cfg_pin_b, sizeof(csvd_config), cudaHostAllocDefault));
     CK(cudaHostAlloc(&ctx->cfg_pin_fixed, sizeof(csvd_config), cudaHostAllocDefault));
@@ -1188,6 +1198,7 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
         if (ctx->k_buffers[i]) cudaFree(ctx->k_buffers[i]);
     if (ctx->flush_buf) cudaFree(ctx->flush_buf);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->h_map) cudaFreeHost(ctx->h_map);
     for (csvd_config *p : {ctx->cfg_pin, ctx->cfg_pin_b, ctx->cfg_pin_fixed})
         if (p) cudaFreeHost(p);
     if (ctx->res_pin) cudaFreeHost(ctx->res_pin);
@@ -1275,7 +1286,8 @@ extern "C" int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config 
     const int d = ctx->D.d;
     const int64_t first = ctx->first_chunk;
     if ((rc = sync_cfg(ctx, cfg, s))) return rc;
-    memcpy(ctx->h_pin, h, sizeof(double) * d);
+    const bool zc = !ctx->direct && ctx->g_host_head && head_config(cfg) && ctx->h_zero_copy;
+    memcpy(zc ? ctx->h_map : ctx->h_pin, h, sizeof(double) * d);
     if (ctx->direct) {
         CK(cudaMemcpyAsync(ctx->d_h, ctx->h_pin, sizeof(double) * d, cudaMemcpyHostToDevice, s));
         if ((rc = launch(ctx, LAUNCH_STEP, s))) return rc;

@@ -62,8 +62,8 @@ static __device__ __forceinline__ double head_bounds(const Dev &D, const double 
     __shared__ double s_qn;
     __shared__ double s_dot[WARPS][MAX_PER_WARP];
     const int G = gridDim.x, stride = G * WARPS;
-    if (warp == WARPS - 1) {  // ||h|| = sqrt(sum(h*h)) (_linalg.py:40-43)
-        const double ss = warp_dot_regular<double, 8, Q>(D.h, hs, D.bplan.leaf_len, lane);
+    if (warp == WARPS - 1) {  // ||h|| = sqrt(sum(h*h)) (_linalg.py:40-43), both operands staged
+        const double ss = warp_selfdot_smem<Q>(hs, D.bplan.leaf_len, lane);
         if (lane == 0) s_qn = __dsqrt_rn(ss);
     }
     int j = 0;

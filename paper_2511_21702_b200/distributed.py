@@ -281,7 +281,7 @@ class ShardedDecoder:
         owned = (np.asarray(plan.assignment) == self.rank)
         if backend is None:
             import torch
-            dev = torch.cuda.current_device() if device is None else device
+            dev = (torch.cuda.current_device() if torch.cuda.is_available() else 0) if device is None else device
             backend = DeviceShard(table, index, owned, dev)
         self.backend = backend
         self.V, self.C, self.d = int(index.vocab_size), int(index.n_clusters), int(index.hidden_dim)

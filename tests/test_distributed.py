@@ -91,3 +91,53 @@ def test_sharded_step_two_ranks_gloo():
     fbs = {fb for _, fb in seen}
     # the query/config mix exercises the merge and every fallback level
     assert {None, "partial_expand", "full_vocab"} <= fbs, seen
+
+
+def _worker_api(rank, world, port, q):
+    """shard.sharded_decode_step(..., group=pg): the opt-in distributed path
+    of the reference call site, with the rank's device work stood in for by
+    the oracle shard; the inputs digest check rejects mismatched queries."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import csvd_oracle as O
+        import paper_2511_21702_b200 as P
+        from paper_2511_21702_b200 import distributed as Dm, shard, workload as wl
+        from shard_oracle import OracleShard
+
+        T = wl.synth_vocab(2000, 64, 10, 0.3, 1)
+        ix = wl.fast_index(T, 10, 2)
+        plan = shard.contiguous_plan(ix, world)
+        Dm.DeviceShard = lambda table, index, owned, dev: OracleShard(table, index, owned)  # no GPU here
+        h = wl.generate_queries(2, 64, "contextual", 7, centroids=ix.centroids)
+        cfg = P.DecodeConfig(k=10)
+        out, ledger = shard.sharded_decode_step(T, ix, plan, h[0], cfg, group=dist.group.WORLD)
+        exp = O.decode_step_batchselect(T, ix, h[0], cfg)
+        assert_outcome(out, _fields(exp), rtol=TRANS_RTOL, where=f"api rank {rank}")
+        assert ledger.bytes_bounds_phase > 0
+        try:  # ranks disagree on the query: refused on every rank
+            shard.sharded_decode_step(T, ix, plan, h[rank], cfg, group=dist.group.WORLD)
+            q.put((rank, "fail", "mismatched queries were accepted"))
+        except ValueError:
+            q.put((rank, "ok", None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+
+
+def test_sharded_decode_step_api_group_opt_in():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_api, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info in res:
+        assert status == "ok", f"rank {rank}:\n{info}"
