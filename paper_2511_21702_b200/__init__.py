@@ -39,6 +39,7 @@ from .engine import (
 )
 from .shard import CommLedger, LatencyModel, ShardPlan, make_plan, sharded_decode_step
 from . import formats
+from .cluster import build_index_gpu
 from .budget import (AdaptiveBudget, BudgetedDecoder, FlopReport, adapt_budget, flop_accounting, flop_report,
                      warmup_k_max)
 
@@ -50,5 +51,5 @@ __all__ = [
     "PartialExpand", "RelaxEps", "StepMetrics", "DeviceIndex", "clear_cache", "cluster_bounds",
     "decode_step", "decode_step_batch", "decode_step_batchselect", "dense_logits", "prepare", "refined_bias_bound", "CommLedger",
     "LatencyModel", "ShardPlan", "make_plan", "sharded_decode_step", "AdaptiveBudget", "BudgetedDecoder",
-    "FlopReport", "adapt_budget", "flop_accounting", "flop_report", "warmup_k_max",
+    "FlopReport", "adapt_budget", "flop_accounting", "flop_report", "warmup_k_max", "build_index_gpu",
 ]
