@@ -662,10 +662,13 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
     // shared batched bounds: regular bound plans (d = 2^m leaves of L % 8 == 0)
     ctx->kbb = nullptr;
     if (D0.bplan.regular && D0.bplan.cpl == 8 && D0.mode != CSVD_MODE_BIAS_AUGMENTED) {
+        const bool pair = getenv("CSVD_KBB_PAIR") ? atoi(getenv("CSVD_KBB_PAIR")) != 0 : D0.C > ctx->grid * WARPS;
         switch (D0.bplan.q) {
-            case 1: ctx->kbb = k_bounds_batch<1>; break;  // fits any d with >= 1 query per pass
-            case 2: ctx->kbb = k_bounds_batch<2>; break;
-            case 4: ctx->kbb = k_bounds_batch<4>; break;
+            // two clusters per warp task (half the shared-memory reads of h) when
+            // the clusters outnumber the warps; else one cluster x 6 queries
+            case 1: ctx->kbb = pair ? k_bounds_batch<1, 2> : k_bounds_batch<1, 1>; break;
+            case 2: ctx->kbb = pair ? k_bounds_batch<2, 2> : k_bounds_batch<2, 1>; break;
+            case 4: ctx->kbb = pair ? k_bounds_batch<4, 2> : k_bounds_batch<4, 1>; break;
         }
     }
     if (ctx->kbb) {

@@ -353,12 +353,25 @@ static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int 
     HF_CAS(a, 1, 3) HF_CAS(a, 4, 6) HF_CAS(a, 5, 7) HF_CAS(a, 1, 2) HF_CAS(a, 5, 6) \
     HF_CAS(a, 0, 4) HF_CAS(a, 3, 7) HF_CAS(a, 1, 5) HF_CAS(a, 2, 6) HF_CAS(a, 1, 4) \
     HF_CAS(a, 3, 6) HF_CAS(a, 2, 4) HF_CAS(a, 3, 5) HF_CAS(a, 3, 4)
-static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o, int hn, double *L,
+static __device__ __forceinline__ int head_certify_fast(const Dev &D, const Ord &o, int hn, double *L,
                                                      csvd_result &res) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const csvd_config &cfg = *D.cfg;
     const int k = cfg.k;
     const int R = o.cum[hn];
+    // certify.py:93-107 with inline libdevice exp / log / division (the same
+    // functions csvd_rho / csvd_delta call out of line: identical values)
+    auto rho_of = [](double log_z, double lr) {
+        if (lr == -INFINITY) return 0.0;
+        if (log_z == -INFINITY) return 1.0;
+        return __ddiv_rn(1.0, __dadd_rn(1.0, exp(__dsub_rn(log_z, lr))));
+    };
+    auto delta_of = [](double log_z, double lr) {
+        if (lr == -INFINITY) return 0.0;
+        if (log_z == -INFINITY) return (double)INFINITY;
+        return exp(__dsub_rn(lr, log_z));
+    };
+    const double dthr = __ddiv_rn(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon));
     __shared__ double s_red[WARPS], s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX], s_wl[WARPS * KH];
     __shared__ int s_p, s_kind;
     __shared__ double s_kth, s_tie;
@@ -462,7 +475,7 @@ static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o,
             if (p <= hn) {
                 s_zq[p - 1] = z;  // Z(p)
                 const long long n = o.cum[p];
-                const double lz = __dadd_rn(M, csvd_log(z));
+                const double lz = __dadd_rn(M, log(z));
                 const double lr = o.lrh[p];
                 int kd = -1;
                 if (n > cfg.k_max) {
@@ -480,8 +493,8 @@ static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o,
                                 }
                             }
                         } else if (t == CSVD_TARGET_SOFTMAX) {
-                            if (n > 0 && csvd_rho(lz, lr) <= cfg.epsilon) kd = CSVD_KIND_SOFTMAX_EPS;
-                        } else if (n > 0 && csvd_delta(lz, lr) <= csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon))) {
+                            if (n > 0 && rho_of(lz, lr) <= cfg.epsilon) kd = CSVD_KIND_SOFTMAX_EPS;
+                        } else if (n > 0 && delta_of(lz, lr) <= dthr) {
                             kd = CSVD_KIND_TOPP_MASS;
                         }
                     }
@@ -493,9 +506,9 @@ static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o,
                 if (n > 0)
                     for (int ti = 0; ti < cfg.n_targets; ++ti) {
                         const int t = cfg.targets[ti];
-                        if (t == CSVD_TARGET_SOFTMAX && near_tie(csvd_rho(lz, lr), cfg.epsilon)) tie_p = min(tie_p, p);
+                        if (t == CSVD_TARGET_SOFTMAX && near_tie(rho_of(lz, lr), cfg.epsilon)) tie_p = min(tie_p, p);
                         if (t == CSVD_TARGET_TOPP &&
-                            near_tie(csvd_delta(lz, lr), csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon))))
+                            near_tie(delta_of(lz, lr), dthr))
                             tie_p = min(tie_p, p);
                     }
             }
@@ -535,19 +548,19 @@ static __device__ __noinline__ int head_certify_fast(const Dev &D, const Ord &o,
         hi = warp_max(hi);
         if (lane == 0) {
             const int n = o.cum[ps];
-            const double lz = __dadd_rn(M, csvd_log(s_zq[ps - 1]));
+            const double lz = __dadd_rn(M, log(s_zq[ps - 1]));
             const double lr = o.lrh[ps];
-            const double rho = csvd_rho(lz, lr);
+            const double rho = rho_of(lz, lr);
             const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
             double xi;
             if (n < 2 || ps >= D.C) xi = NAN;
-            else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+            else xi = (um <= lo) ? 1.0 : __ddiv_rn(__dsub_rn(hi, lo), __dsub_rn(um, lo));
             double eps_ach = 0.0;
             if (kind == CSVD_KIND_SOFTMAX_EPS) {
                 eps_ach = rho;
             } else if (kind == CSVD_KIND_TOPP_MASS) {
-                const double dl = csvd_delta(lz, lr);
-                eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+                const double dl = delta_of(lz, lr);
+                eps_ach = isfinite(dl) ? __ddiv_rn(dl, __dadd_rn(1.0, dl)) : 1.0;
             }
             memset(&res, 0, sizeof(res));
             res.kind = kind;

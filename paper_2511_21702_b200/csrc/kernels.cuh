@@ -1866,7 +1866,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_step(const __grid_constant__ Dev
 // ---------------------------------------------------------------------------
 #define BQN 3   // queries per register block when a warp pairs two clusters
 #define BQN1 6  // queries per register block at one cluster per warp (C <= warps)
-template <int BQ>
+template <int BQ, int NR = 1>
 __global__ void __launch_bounds__(THREADS, 1)
     k_bounds_batch(Dev D, const double *__restrict__ H, int B, double *const *Uraw_l, double *const *dots_l,
                    csvd_result *res_all, int gq /* queries per pass (<= BQN1, by shared memory) */) {
@@ -1885,15 +1885,37 @@ __global__ void __launch_bounds__(THREADS, 1)
         // one cluster per warp task (looping over the clusters), the
         // registers a second row would take hold more queries instead; the
         // row's next element step is in flight while the current one is used
+        if constexpr (NR == 1) {
 #pragma unroll 1
-        for (int c = gwarp; c < D.C; c += nwarps) {
-            const double *const rows[1] = {D.cent + (size_t)c * D.bd};
-            double dots[1][BQN1];
-            warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
-            if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
+            for (int c = gwarp; c < D.C; c += nwarps) {
+                const double *const rows[1] = {D.cent + (size_t)c * D.bd};
+                double dots[1][BQN1];
+                warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
+                if (lane == 0) {  // the lanes finish U = dot + R ||h|| (+ max b) themselves
 #pragma unroll
-                for (int j = 0; j < BQN1; ++j)
-                    if (j < nq) dots_l[qb + j][c] = dots[0][j];
+                    for (int j = 0; j < BQN1; ++j)
+                        if (j < nq) dots_l[qb + j][c] = dots[0][j];
+                }
+            }
+        } else {  // two clusters x BQN queries: every staged h value feeds both rows
+#pragma unroll 1
+            for (int c = gwarp; c < D.C; c += 2 * nwarps) {
+                const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
+                const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
+#pragma unroll 1
+                for (int j0 = 0; j0 < nq; j0 += BQN) {
+                    double dots[2][BQN];
+                    warp_dot_regular_multi<BQ, BQN, 2>(rows, smem + (size_t)j0 * hs_stride, hs_stride,
+                                                       min(BQN, nq - j0), D.bplan.leaf_len, lane, dots);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < BQN; ++j)
+                            if (j0 + j < nq) {
+                                dots_l[qb + j0 + j][c] = dots[0][j];
+                                if (c2 != c) dots_l[qb + j0 + j][c2] = dots[1][j];
+                            }
+                    }
+                }
             }
         }
         __syncthreads();
