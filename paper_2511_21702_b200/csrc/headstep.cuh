@@ -115,7 +115,7 @@ static __device__ __forceinline__ bool head_fits(const Dev &D, const Ord &o, int
 //     top-k values (k pops of the lanes' running maxima)
 //   warp 0: every prefix's tests at once -> the decision prefix ps, whose
 //     k-th value is a k-pop merge of the first ps clusters' lists
-static __device__ __noinline__ int head_certify(const Dev &D, const Ord &o, int hn, double *L, csvd_result &res) {
+static __device__ __forceinline__ int head_certify(const Dev &D, const Ord &o, int hn, double *L, csvd_result &res) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const csvd_config &cfg = *D.cfg;
     const int k = cfg.k;
@@ -838,27 +838,33 @@ __global__ void __launch_bounds__(THREADS, 1) k_head(const __grid_constant__ Dev
 // into the Dev (all table data is shared); bounds come from k_bounds_batch
 template <typename ET, int Q>
 __global__ void __launch_bounds__(THREADS, 1) k_head_lanes(const __grid_constant__ Dev D0) {
-    Dev D = D0;
-    const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
-    D.h = w.h;
-    D.U = w.U;
-    D.Uraw = w.Uraw;
-    D.dots = w.dots;
-    D.order_g = w.order_g;
-    D.cum_g = w.cum_g;
-    D.S_logits = w.S_logits;
-    D.S_ids = w.S_ids;
-    D.st = w.st;
-    D.res = w.res;
-    D.bar = w.bar;
-    D.cand = w.cand;
-    D.klists = w.klists;
-    D.shard_out = w.shard_out;
-    D.res_host = w.res_host;
-    D.ids_host = w.ids_host;
-    D.logits_host = w.logits_host;
-    D.hcnt = w.hcnt;
-    D.bar64 = w.bar64;
-    D.dbg = nullptr;
+    // the lane's Dev lives in shared memory: a local copy would sit in local
+    // memory, whose L1 lines every acquire / fence of the step invalidates
+    __shared__ Dev D;
+    if (threadIdx.x == 0) {
+        const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
+        D = D0;
+        D.h = w.h;
+        D.U = w.U;
+        D.Uraw = w.Uraw;
+        D.dots = w.dots;
+        D.order_g = w.order_g;
+        D.cum_g = w.cum_g;
+        D.S_logits = w.S_logits;
+        D.S_ids = w.S_ids;
+        D.st = w.st;
+        D.res = w.res;
+        D.bar = w.bar;
+        D.cand = w.cand;
+        D.klists = w.klists;
+        D.shard_out = w.shard_out;
+        D.res_host = w.res_host;
+        D.ids_host = w.ids_host;
+        D.logits_host = w.logits_host;
+        D.hcnt = w.hcnt;
+        D.bar64 = w.bar64;
+        D.dbg = nullptr;
+    }
+    __syncthreads();
     if (head_path<ET, Q, true>(D)) step_body<ET, 8, Q, 8, Q>(D);
 }

@@ -349,7 +349,7 @@ __device__ __forceinline__ double cone_bound(const Dev &D, int c, double dot, do
 }
 
 // U from a centroid dot (batch lanes; off the single-query path, so out of line)
-static __device__ __noinline__ double bound_from_dot(const Dev &D, int c, double dot, double qn) {
+static __device__ __forceinline__ double bound_from_dot(const Dev &D, int c, double dot, double qn) {
     if (D.mode == CSVD_MODE_SPHERICAL) return cone_bound(D, c, dot, qn);
     return __dadd_rn(__dadd_rn(dot, __dmul_rn(D.radii[c], qn)), D.maxb[c]);
 }
@@ -1829,26 +1829,31 @@ template <typename ET, int CPL, int Q, int BCPL, int BQ, bool GROUPED = false>
 __global__ void __launch_bounds__(THREADS, 1) k_step(const __grid_constant__ Dev D0) {
     if constexpr (GROUPED) {
         // one launch runs a whole batch: lane b is blockIdx.x / nblocks and
-        // swaps its own workspaces into the Dev (all table data is shared)
-        Dev D = D0;
-        const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
-        D.h = w.h;
-        D.U = w.U;
-        D.Uraw = w.Uraw;
-        D.dots = w.dots;
-        D.order_g = w.order_g;
-        D.cum_g = w.cum_g;
-        D.S_logits = w.S_logits;
-        D.S_ids = w.S_ids;
-        D.st = w.st;
-        D.res = w.res;
-        D.bar = w.bar;
-        D.cand = w.cand;
-        D.klists = w.klists;
-        D.shard_out = w.shard_out;
-        D.res_host = w.res_host;
-        D.ids_host = w.ids_host;
-        D.logits_host = w.logits_host;
+        // swaps its own workspaces into the Dev (all table data is shared);
+        // the lane's Dev lives in shared memory, not local memory
+        __shared__ Dev D;
+        if (threadIdx.x == 0) {
+            const LaneWS &w = D0.lanes[blockIdx.x / (unsigned)D0.nblocks];
+            D = D0;
+            D.h = w.h;
+            D.U = w.U;
+            D.Uraw = w.Uraw;
+            D.dots = w.dots;
+            D.order_g = w.order_g;
+            D.cum_g = w.cum_g;
+            D.S_logits = w.S_logits;
+            D.S_ids = w.S_ids;
+            D.st = w.st;
+            D.res = w.res;
+            D.bar = w.bar;
+            D.cand = w.cand;
+            D.klists = w.klists;
+            D.shard_out = w.shard_out;
+            D.res_host = w.res_host;
+            D.ids_host = w.ids_host;
+            D.logits_host = w.logits_host;
+        }
+        __syncthreads();
         step_body<ET, CPL, Q, BCPL, BQ>(D);
     } else {
         if (D0.dbg && threadIdx.x == 0) D0.dbg[128 + blockIdx.x] = gtimer();
