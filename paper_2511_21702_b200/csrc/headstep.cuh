@@ -55,6 +55,25 @@ static __device__ __forceinline__ unsigned long long grid_sync_mono(const Dev &D
     return epoch;  // thread 0: this barrier's epoch (1, 2, ... over the counter's life)
 }
 
+// release / acquire primitives (GPU scope).  A release by one thread after a
+// __syncthreads() also orders the other threads' earlier writes (the barrier
+// makes them visible to it; release is cumulative), so a CTA publishes its
+// rows with one release operation instead of full SC fences (__threadfence
+// compiles to MEMBAR.SC.GPU + an L1 invalidation on this part).
+static __device__ __forceinline__ void red_release_add(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+static __device__ __forceinline__ int ld_acquire_s32(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+static __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // bounds for this CTA's clusters (warp per cluster, as bounds_phase) and ||h||
 template <int Q>
 static __device__ __forceinline__ double head_bounds(const Dev &D, const double *hs) {
@@ -687,8 +706,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                 }
             }
         }
-        if (lane == 0) __threadfence();
-        __syncthreads();
+        __syncthreads();  // the rows are published by the release operations below
         if (D.dbg && tid == 0) D.dbg[384 + (b & 255)] = gtimer();
         if (D.res_host) {  // host-API step: this CTA's rows into the mapped buffers (speculative:
                            // the host reads only the first |S| entries)
@@ -700,18 +718,12 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         if (G > 1) {  // this CTA's share of every cluster it touches (release: rows visible first)
             if (tid < hn) {
                 const int a = max(o.cum[tid], r_lo), e = min(o.cum[tid + 1], r_hi);
-                if (e > a) {
-                    __threadfence();
-                    atomicAdd(D.hcnt + tid, e - a);
-                }
+                if (e > a) red_release_add(D.hcnt + tid, e - a);
             }
             __syncthreads();
         }
         if (b > 0) {  // then its arrival, and CTA 0's decision
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(D.hcnt + HMAX, 1);
-            }
+            if (tid == 0) red_release_add(D.hcnt + HMAX, 1);
             // ---- wait for CTA 0's decision
             __shared__ int s_dec;
             if (tid == 0) {
@@ -728,7 +740,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                     }
                     __nanosleep(256);
                 }
-                __threadfence();
+                (void)ld_acquire_u64(decision);  // acquire: CTA 0's result is ordered before what follows
                 s_dec = (int)(v & 1);
                 if (D.dbg && b < 256) D.dbg[128 + b] = gtimer();
             }
@@ -750,9 +762,9 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                     break;
                 }
             } while (v < n);
+            (void)ld_acquire_s32(ctr);  // acquire: the counted rows are visible to this CTA after the barrier
         }
         __syncthreads();
-        __threadfence();
     }
     if (lead) DBG_TS(D, 29);
     if (D.dbg && tid == 0 && b == 0) {  // debug calibration: 256 dependent f64 adds on this SM
@@ -819,7 +831,6 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             *D.st = s2;
             if (D.res_host) *D.res_host = r;
         }
-        __threadfence();
         if constexpr (GROUPED) D.bar64[0] = epoch;  // the lane's step count (read before the next step)
         const unsigned long long w = epoch * 2 + (decided ? 1 : 0);
         asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(decision), "l"(w) : "memory");

@@ -1444,9 +1444,15 @@ static __device__ __noinline__ void publish_host(const Dev &D, long long n, cons
     if (!D.res_host) return;
     const long long per = (n + CTA_N - 1) / CTA_N;
     const long long a = (long long)CTA_ID * per, b = min(n, a + per);
+    // the fields once (a reference parameter of an out-of-line function is read
+    // through generic loads, which the loop would otherwise repeat)
+    long long *__restrict__ ih = D.ids_host;
+    double *__restrict__ lh = D.logits_host;
+    const long long *__restrict__ is = D.S_ids;
+    const double *__restrict__ ls = D.S_logits;
     for (long long i = a + threadIdx.x; i < b; i += THREADS) {
-        D.ids_host[i] = __ldcg(D.S_ids + i);
-        D.logits_host[i] = __ldcg(D.S_logits + i);
+        ih[i] = __ldcg(is + i);
+        lh[i] = __ldcg(ls + i);
     }
     if (CTA_ID == 0 && threadIdx.x == 0) *D.res_host = *r_cta0;
 }
