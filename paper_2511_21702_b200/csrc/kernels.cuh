@@ -294,22 +294,28 @@ __device__ __forceinline__ bool key_before(double ua, int ia, double ub, int ib)
 static __device__ __forceinline__ void grid_sync(const Dev &D) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned gen = ld_acquire(D.bar + 1);
-        __threadfence();
-        const unsigned t = atomicAdd(D.bar, 1u);
+        // acq_rel arrival (releases this CTA's writes, which the barrier above
+        // made visible to this thread; cumulative), relaxed polling, one
+        // acquire at the end: no SC fences
+        unsigned gen, t;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(D.bar + 1) : "memory");
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(D.bar) : "memory");
         if (t == (unsigned)D.nblocks - 1u) {
             D.bar[0] = 0;
-            __threadfence();
             st_release(D.bar + 1, gen + 1u);
         } else {
             unsigned long long spins = 0;
-            while (ld_acquire(D.bar + 1) == gen) {
+            unsigned v;
+            while (true) {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.bar + 1) : "memory");
+                if (v != gen) break;
                 __nanosleep(CSVD_SPIN_NS);
                 if (++spins > (1ull << 24)) {  // ~1-2 s: flag and give up rather than hang
                     D.res->error = CSVD_ESTATE;
                     break;
                 }
             }
+            (void)ld_acquire(D.bar + 1);
         }
     }
     __syncthreads();
@@ -1725,8 +1731,7 @@ __device__ __forceinline__ void step_body(const Dev &D) {    extern __shared__ _
                     cluster_summary(D, o.cum[q], o.cum[q + 1], k, D.gsum + 3 * D.C + (size_t)q * 32, D.gsum + q,
                                     D.gsum + D.C + q, D.gsum + 2 * D.C + q, pre, lane);
                 }
-                if (lane == 0) __threadfence();
-                grid_sync(D);
+                grid_sync(D);  // its acq_rel arrival publishes the summaries
             }
             // summaries + scan, chunk by chunk (identical in every CTA)
             for (int q0 = st.p_lo; q0 < st.p_hi; q0 += D.chunk) {
