@@ -634,8 +634,8 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
             return rc;
         CK(cudaMemset(L.bar, 0, 16));
         CK(cudaMemset(L.st, 0, sizeof(ScanState)));
-        if ((rc = lalloc(ctx, &L.hcnt, (size_t)HMAX + 1)) || (rc = lalloc(ctx, &L.bar64, 4))) return rc;
-        CK(cudaMemset(L.hcnt, 0, sizeof(int) * (HMAX + 1)));
+        if ((rc = lalloc(ctx, &L.hcnt, (size_t)HW_TOTAL_INTS)) || (rc = lalloc(ctx, &L.bar64, 4))) return rc;
+        CK(cudaMemset(L.hcnt, 0, sizeof(int) * HW_TOTAL_INTS));
         CK(cudaMemset(L.bar64, 0, 32));
         L.nblocks = G;
         L.gsum = nullptr;  // distributed wave summaries: single-step contexts only
@@ -1137,8 +1137,8 @@ static int create_impl(csvd_ctx **out, int device, const csvd_table_desc *t, con
     if ((rc = dalloc(ctx, &D.bar, 4))) return rc;
     CK(cudaMemset(D.bar, 0, 16));
     if ((rc = dalloc(ctx, &D.gsum, (size_t)D.C * (3 + 32)))) return rc;
-    if ((rc = dalloc(ctx, &D.hcnt, (size_t)HMAX + 1))) return rc;
-    CK(cudaMemset(D.hcnt, 0, sizeof(int) * (HMAX + 1)));
+    if ((rc = dalloc(ctx, &D.hcnt, (size_t)HW_TOTAL_INTS))) return rc;
+    CK(cudaMemset(D.hcnt, 0, sizeof(int) * HW_TOTAL_INTS));
     if ((rc = dalloc(ctx, &D.bar64, 2))) return rc;
     CK(cudaMemset(D.bar64, 0, 16));
     CK(cudaMemset(D.st, 0, sizeof(ScanState)));
@@ -1236,7 +1236,7 @@ static int result_error(csvd_ctx *ctx, const csvd_result &r) {
     if (r.error == CSVD_EVALUE) return fail(ctx, CSVD_EVALUE, "bounds must be finite");
     cudaMemset(ctx->D.bar, 0, 16);  // a timed-out barrier leaves stale counts
     cudaMemset(ctx->D.bar64, 0, 16);
-    cudaMemset(ctx->D.hcnt, 0, sizeof(int) * (HMAX + 1));
+    cudaMemset(ctx->D.hcnt, 0, sizeof(int) * HW_INTS);
     return fail(ctx, r.error, "device state error (grid barrier timeout)");
 }
 

@@ -30,6 +30,22 @@
 #define HMAX 64  // head clusters (order_head's limit)
 #define KH 32    // k limit of the head kernel (the scan's register lists)
 
+// Head workspace (D.hcnt, one allocation per step context / batch lane):
+//   ints [0, HMAX]            arrivals of the row CTAs at [HMAX]
+//   ints [HW_HIST, +HMAX + 2) top-k histogram (certify.py:128-139 as counts)
+//   HeadRec [HW_SEGS]         per-(row CTA b, cluster position q) segment records, slot b + q
+#define HW_INTS 256
+#define HW_HIST 80
+#define HW_SEGS 256
+#define HW_TOTAL_INTS (HW_INTS + HW_SEGS * 8)
+struct HeadRec {
+    double z, mn, mx;  // sum exp(S - est), min, max over the segment's logits
+    int q;             // cluster position in the opening order
+    unsigned ep;       // the step's epoch (stale records never match)
+};
+static_assert(sizeof(HeadRec) == 32, "HeadRec layout");
+__device__ __forceinline__ HeadRec *hw_recs(const Dev &D) { return reinterpret_cast<HeadRec *>(D.hcnt + HW_INTS); }
+
 // Grid barrier on a monotone 64-bit arrival counter: one atomic per CTA and
 // no reset (the target is the next multiple of the grid size), so a barrier is
 // one L2 round trip plus the arrival of the slowest CTA.  Only kernels with
@@ -601,6 +617,281 @@ static __device__ __forceinline__ int head_certify_fast(const Dev &D, const Ord 
 #undef HF_SORT8
 #undef HF_CAS
 
+// Certification from the row CTAs' records (CTA 0).  The per-logit work of
+// certify.py:73-88 / 128-139 (exp sums, extrema, the top-k histogram) was done
+// by the row CTAs as their rows finished; this reduces the segment records per
+// cluster in a fixed order, tests every head prefix at once (as head_certify)
+// and selects the decision prefix's k-th logit (np.partition, certify.py:88)
+// among the logits at or above the k-th largest segment maximum (at least k
+// logits reach it, so the k-th logit does too).
+//   log Z_S(p) = est + log(sum over the first p clusters of sum exp(S - est))
+//   (est: the best-logit estimate; the max-shifted form's value within ulps)
+// The code is deliberately compact (rolled loops, out-of-line libdevice
+// calls): it runs once per step on one SM, cold after the rest of the model,
+// and its instruction fetch -- not its arithmetic -- is what it costs.
+// Returns 1 decided, 0 general path, -1 the records cannot decide (a sum out
+// of range, too many candidates): head_certify works from S instead.
+static __device__ __noinline__ int seg_prefix_kind(const csvd_config *cfgp, int Cn, int p, long long n, int c,
+                                                   double lz, double lr, int *tie) {
+    const csvd_config &cfg = *cfgp;
+    const double dthr = csvd_ddiv(cfg.epsilon, __dsub_rn(1.0, cfg.epsilon));
+    int kd = -1, t2 = 0;
+    if (n > cfg.k_max) kd = 99;  // budget overflow: the fallback chain (general path)
+#pragma unroll 1
+    for (int ti = 0; ti < cfg.n_targets; ++ti) {
+        const int t = cfg.targets[ti];
+        if (t == CSVD_TARGET_TOPK) {
+            if (kd < 0 && n >= cfg.k && (p >= Cn || c >= cfg.k)) kd = CSVD_KIND_TOPK_EXACT;
+        } else if (n > 0) {
+            const bool sm = t == CSVD_TARGET_SOFTMAX;
+            const double v = sm ? csvd_rho(lz, lr) : csvd_delta(lz, lr);
+            const double thr = sm ? cfg.epsilon : dthr;
+            if (kd < 0 && v <= thr) kd = sm ? CSVD_KIND_SOFTMAX_EPS : CSVD_KIND_TOPP_MASS;
+            t2 |= near_tie(v, thr);
+        }
+    }
+    *tie = t2;
+    return kd;
+}
+
+static __device__ __forceinline__ int head_certify_seg(const Dev &D, const Ord &o, int hn, int Gr, unsigned ep,
+                                                    double est, double *scratch, int scratch_n, csvd_result &res) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = D.cfg->k;
+    const HeadRec *rec = hw_recs(D);
+    __shared__ double s_zq[HMAX], s_mnq[HMAX], s_mxq[HMAX];
+    __shared__ int s_hist[HMAX + 2];
+    __shared__ int s_p, s_kind, s_tie, s_nc;
+    __shared__ double s_T;
+    if (tid <= hn) s_hist[tid] = __ldcg(D.hcnt + HW_HIST + tid);
+    if (tid == 0) {
+        s_nc = 0;
+        s_T = -INFINITY;
+    }
+    // per cluster q (warp q % WARPS): its records sit in slots q + b, b < Gr
+#pragma unroll 1
+    for (int q = warp; q < hn; q += WARPS) {
+        double z = 0.0, mn = INFINITY, mx = -INFINITY;
+        // all of a lane's record loads in flight at once (Gr <= 160 at 148 SMs)
+#pragma unroll 1
+        for (int b0 = lane; b0 < Gr; b0 += 5 * 32) {
+            double2 a[5], c[5];
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const int b = b0 + 32 * j;
+                const double2 *r = reinterpret_cast<const double2 *>(rec + q + min(b, Gr - 1));
+                a[j] = __ldcg(r);
+                c[j] = __ldcg(r + 1);
+            }
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const unsigned long long tag = (unsigned long long)__double_as_longlong(c[j].y);
+                if (b0 + 32 * j < Gr && (unsigned)(tag >> 32) == ep && (int)(unsigned)tag == q) {
+                    z = __dadd_rn(z, a[j].x);
+                    mn = fmin(mn, a[j].y);
+                    mx = fmax(mx, c[j].x);
+                }
+            }
+        }
+#pragma unroll 1
+        for (int off = 16; off; off >>= 1) {
+            z = __dadd_rn(z, __shfl_xor_sync(CSVD_FULL, z, off));
+            mn = fmin(mn, __shfl_xor_sync(CSVD_FULL, mn, off));
+            mx = fmax(mx, __shfl_xor_sync(CSVD_FULL, mx, off));
+        }
+        if (lane == 0) {
+            s_zq[q] = z;
+            s_mnq[q] = mn;
+            s_mxq[q] = mx;
+        }
+    }
+    __syncthreads();
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 53);
+    // ---- every prefix at once (warp 0: lane l tests p = l + 1 and l + 33)
+    if (warp == 0) {
+        int carry = 0;
+        double zc = 0.0;
+        int first = 0x7fffffff, kind = -1, tie_p = 0x7fffffff, bad = 0;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int p = lane + 1 + 32 * h;
+            int c = p <= hn ? s_hist[p] : 0;
+            double z = p <= hn ? s_zq[p - 1] : 0.0;
+#pragma unroll 1
+            for (int off = 1; off < 32; off <<= 1) {
+                const int u = __shfl_up_sync(CSVD_FULL, c, off);
+                const double w = __shfl_up_sync(CSVD_FULL, z, off);
+                if (lane >= off) {
+                    c += u;
+                    z = __dadd_rn(z, w);
+                }
+            }
+            c += carry;
+            z = __dadd_rn(z, zc);
+            carry = __shfl_sync(CSVD_FULL, c, 31);
+            zc = __shfl_sync(CSVD_FULL, z, 31);
+            if (p <= hn) {
+                s_zq[p - 1] = z;  // now Z(p)
+                bad |= !(z > 1e-290 && z < 1e290);
+                int tie;
+                const int kd = seg_prefix_kind(D.cfg, D.C, p, o.cum[p], c, __dadd_rn(est, csvd_log(z)), o.lrh[p], &tie);
+                if (kd >= 0 && p < first) {
+                    first = p;
+                    kind = kd;
+                }
+                if (tie) tie_p = min(tie_p, p);
+            }
+        }
+#pragma unroll 1
+        for (int off = 16; off; off >>= 1) {
+            const int f2 = __shfl_xor_sync(CSVD_FULL, first, off), k2 = __shfl_xor_sync(CSVD_FULL, kind, off);
+            if (f2 < first) {
+                first = f2;
+                kind = k2;
+            }
+        }
+        tie_p = __reduce_min_sync(CSVD_FULL, (unsigned)tie_p);
+        bad = __any_sync(CSVD_FULL, bad);
+        if (lane == 0) {
+            s_p = bad ? -1 : first;
+            s_kind = kind;
+            s_tie = tie_p <= first;
+        }
+    }
+    __syncthreads();
+    const int ps = s_p, kind = s_kind;
+    if (DBG_HERE(D) && tid == 0) DBG_TS(D, 54);
+    if (ps < 0) return -1;
+    if (ps > hn || kind == 99) return 0;
+    const int n = o.cum[ps];
+    double kth = -INFINITY;
+    if (n >= k && scratch_n < THREADS + 64) return -1;
+    if (n >= k) {
+        // T = the k-th largest maximum among the segments of clusters < ps
+        // (slot s = b + q, at most Gr + hn <= HW_SEGS <= THREADS of them)
+        double *sm = scratch, *cl = scratch + THREADS;
+        const int cap = min(2048, scratch_n - THREADS);
+        double m = -INFINITY;
+        if (tid < Gr + hn) {
+            const double2 c = __ldcg(reinterpret_cast<const double2 *>(rec + tid) + 1);
+            const unsigned long long tag = (unsigned long long)__double_as_longlong(c.y);
+            if ((unsigned)(tag >> 32) == ep && (int)(unsigned)tag < ps) m = c.x;
+        }
+        sm[tid] = m;
+        __syncthreads();
+        if (m != -INFINITY) {
+            int rank = 0;
+#pragma unroll 4
+            for (int j = 0; j < Gr + hn; ++j) {
+                const double w = sm[j];
+                rank += (w > m || (w == m && j < tid)) ? 1 : 0;
+            }
+            if (rank == k - 1) s_T = m;
+        }
+        __syncthreads();
+        // candidates: the first n logits at or above T (at least k of them)
+        const double T = s_T;
+#pragma unroll 1
+        for (int i0 = tid; i0 < n; i0 += 8 * THREADS) {
+            double x[8];  // eight loads in flight
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = __ldcg(D.S_logits + min(i0 + j * THREADS, n - 1));
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j)
+                if (i0 + j * THREADS < n && x[j] >= T) {
+                    const int slot = atomicAdd(&s_nc, 1);
+                    if (slot < cap) cl[slot] = x[j];
+                }
+        }
+        __syncthreads();
+        const int nc = s_nc;
+        if (nc > cap || nc < k) return -1;
+        if (nc <= THREADS) {  // one candidate per thread: its rank by counting
+            if (tid < nc) {
+                const double v = cl[tid];
+                int rank = 0;
+#pragma unroll 4
+                for (int j = 0; j < nc; ++j) {
+                    const double w = cl[j];
+                    rank += (w > v || (w == v && j < tid)) ? 1 : 0;
+                }
+                if (rank == k - 1) s_T = v;
+            }
+            __syncthreads();
+            kth = s_T;
+        } else {
+        // bitonic sort (descending) of the candidates, padded to a power of two
+        int m2 = 32;
+        while (m2 < nc) m2 <<= 1;
+        for (int i = nc + tid; i < m2; i += THREADS) cl[i] = -INFINITY;
+        __syncthreads();
+#pragma unroll 1
+        for (int size = 2; size <= m2; size <<= 1) {
+#pragma unroll 1
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll 1
+                for (int i = tid; i < (m2 >> 1); i += THREADS) {
+                    const int a = 2 * i - (i & (stride - 1)), bq = a + stride;
+                    const double va = cl[a], vb = cl[bq];
+                    if ((va < vb) == ((a & size) == 0)) {
+                        cl[a] = vb;
+                        cl[bq] = va;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        kth = cl[k - 1];
+        }
+    }
+    if (warp == 0) {
+        double lo = INFINITY, hi = -INFINITY;
+        if (lane < ps) {
+            lo = s_mnq[lane];
+            hi = s_mxq[lane];
+        }
+        if (lane + 32 < ps) {
+            lo = fmin(lo, s_mnq[lane + 32]);
+            hi = fmax(hi, s_mxq[lane + 32]);
+        }
+#pragma unroll 1
+        for (int off = 16; off; off >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(CSVD_FULL, lo, off));
+            hi = fmax(hi, __shfl_xor_sync(CSVD_FULL, hi, off));
+        }
+        if (lane == 0) {
+            const double lz = __dadd_rn(est, csvd_log(s_zq[ps - 1]));
+            const double lr = o.lrh[ps];
+            const double rho = csvd_rho(lz, lr);
+            const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
+            double xi;
+            if (n < 2 || ps >= D.C) xi = NAN;
+            else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+            double eps_ach = 0.0;
+            if (kind == CSVD_KIND_SOFTMAX_EPS) {
+                eps_ach = rho;
+            } else if (kind == CSVD_KIND_TOPP_MASS) {
+                const double dl = csvd_delta(lz, lr);
+                eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+            }
+            memset(&res, 0, sizeof(res));
+            res.kind = kind;
+            res.fallback = CSVD_FB_NONE;
+            res.sub_size = n;
+            res.clusters_opened = ps;
+            res.heap_pops = ps;
+            res.epsilon_achieved = eps_ach;
+            res.u_max = um;
+            res.topk_min = kth;
+            res.rho = rho;
+            res.xi = xi;
+            res.flags = s_tie ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
+        }
+    }
+    __syncthreads();
+    return 1;
+}
+
 // The head path; returns true when the step needs the general path (every
 // CTA of the grid / lane returns the same), which the caller then runs from
 // scratch: one call site, so one copy of its code, after the head path's.
@@ -615,6 +906,8 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     __shared__ ScanShared ss;
     __shared__ unsigned long long s_hbar, s_epoch;
     __shared__ double s_qn;
+    __shared__ int s_hist[HMAX + 2];  // this CTA's top-k histogram counts
+    for (int i = tid; i < HMAX + 2; i += THREADS) s_hist[i] = 0;
     const bool lead = b == 0 && tid == 0;
     if (lead) DBG_TS(D, 24);
     if (tid == 0) {
@@ -668,10 +961,24 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     const int R = o.cum[hn];
     // small lanes (G <= 3 CTAs): CTA 0 computes rows too, then certifies
     const bool cta0_rows = G <= 3;
+    const int Gr = cta0_rows ? G : G - 1;          // row CTAs
+    const bool segs = Gr + hn <= HW_SEGS;          // segment records fit (always at 148 CTAs)
     if (b > 0 || cta0_rows) {
         // ---- rows of the head, contiguous per row CTA
-        const int rb = cta0_rows ? b : b - 1, Gr = cta0_rows ? G : G - 1;
+        const int rb = cta0_rows ? b : b - 1;
         const int r_lo = (int)((long long)R * rb / Gr), r_hi = (int)((long long)R * (rb + 1) / Gr);
+        // top-k histogram (certify.py:128-139 as counts): a logit x of cluster
+        // position q counts for every prefix p >= max(q + 1, c + 1),
+        // c = #{p in [1, hnu] : Uo[p] >= x}
+        const int hnu = min(hn, D.C - 1);
+        auto tally = [&](double x, int q) {
+            int c = 0;
+#pragma unroll
+            for (int step = 64; step; step >>= 1)
+                if (c + step <= hnu && o.Uo[c + step] >= x) c += step;
+            const int st = max(q + 1, c + 1);
+            if (st <= hn) atomicAdd(&s_hist[st], 1);
+        };
         // two rows per warp at a time (r, r + WARPS): both in flight, h read once
         auto locate = [&](int r, int &wrow, int &pos) {
             int lo = 0, hi = hn;  // cum[lo] <= r < cum[lo+1]
@@ -683,14 +990,15 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             const int i = r - o.cum[lo];
             pos = __ldg(D.starts + c) + i;
             wrow = __ldg(D.wrow0 + c) + i;
+            return lo;
         };
         const ET *Wt = reinterpret_cast<const ET *>(D.W);
 #pragma unroll 1
         for (int r = r_lo + warp; r < r_hi; r += 2 * WARPS) {
             const int r2 = r + WARPS;
-            int wa, pa, wb, pb;
-            locate(r, wa, pa);
-            if (r2 < r_hi) locate(r2, wb, pb);
+            int wa, pa, wb, pb, qb = 0;
+            const int qa = locate(r, wa, pa);
+            if (r2 < r_hi) qb = locate(r2, wb, pb);
             else {
                 wb = wa;
                 pb = pa;
@@ -698,15 +1006,60 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             double la, lb;
             warp_dot_r8_x2<ET, Q>(Wt + (size_t)wa * D.d, Wt + (size_t)wb * D.d, hs, D.wplan.leaf_len, lane, la, lb);
             if (lane == 0) {
-                D.S_logits[r] = __dadd_rn(la, __ldg(D.bias + pa));
+                const double xa = __dadd_rn(la, __ldg(D.bias + pa));
+                D.S_logits[r] = xa;
                 D.S_ids[r] = __ldg(D.perm + pa);
+                if (segs) tally(xa, qa);
                 if (r2 < r_hi) {
-                    D.S_logits[r2] = __dadd_rn(lb, __ldg(D.bias + pb));
+                    const double xb = __dadd_rn(lb, __ldg(D.bias + pb));
+                    D.S_logits[r2] = xb;
                     D.S_ids[r2] = __ldg(D.perm + pb);
+                    if (segs) tally(xb, qb);
                 }
             }
         }
         __syncthreads();  // the rows are published by the release operations below
+        if (segs) {
+            // this CTA's histogram counts (integer adds: order-independent) and
+            // one record per cluster its rows touch, reduced in a fixed order
+            if (tid <= hn && s_hist[tid]) atomicAdd(D.hcnt + HW_HIST + tid, s_hist[tid]);
+            if (r_hi > r_lo) {
+                auto cluster_of = [&](int r) {
+                    int lo = 0, hi = hn;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (o.cum[mid] <= r) lo = mid; else hi = mid;
+                    }
+                    return lo;
+                };
+                const int qa = cluster_of(r_lo), qz = cluster_of(r_hi - 1);
+                const double est = s_est;
+                const unsigned ep = (unsigned)s_epoch;
+#pragma unroll 1
+                for (int q = qa + warp; q <= qz; q += WARPS) {
+                    const int a = max(o.cum[q], r_lo), e = min(o.cum[q + 1], r_hi);
+                    double z = 0.0, mn = INFINITY, mx = -INFINITY;
+#pragma unroll 1
+                    for (int i = a + lane; i < e; i += 32) {
+                        const double x = __ldcg(D.S_logits + i);
+                        // x - est > 700 (never for a sane index) makes z huge: the certifier's range check
+                        z = __dadd_rn(z, exp_nonpos(fmin(__dsub_rn(x, est), 700.0)));
+                        mn = fmin(mn, x);
+                        mx = fmax(mx, x);
+                    }
+                    z = warp_sum(z);
+                    mn = warp_min(mn);
+                    mx = warp_max(mx);
+                    if (lane == 0) {
+                        double2 *rp = reinterpret_cast<double2 *>(hw_recs(D) + rb + q);
+                        const unsigned long long tag = ((unsigned long long)ep << 32) | (unsigned)q;
+                        rp[0] = make_double2(z, mn);
+                        rp[1] = make_double2(mx, __longlong_as_double((long long)tag));
+                    }
+                }
+            }
+            __syncthreads();
+        }
         if (D.dbg && tid == 0) D.dbg[384 + (b & 255)] = gtimer();
         if (D.res_host) {  // host-API step: this CTA's rows into the mapped buffers (speculative:
                            // the host reads only the first |S| entries)
@@ -715,14 +1068,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                 D.ids_host[r] = __ldcg(D.S_ids + r);
             }
         }
-        if (G > 1) {  // this CTA's share of every cluster it touches (release: rows visible first)
-            if (tid < hn) {
-                const int a = max(o.cum[tid], r_lo), e = min(o.cum[tid + 1], r_hi);
-                if (e > a) red_release_add(D.hcnt + tid, e - a);
-            }
-            __syncthreads();
-        }
-        if (b > 0) {  // then its arrival, and CTA 0's decision
+        if (b > 0) {  // its arrival (release: rows, records and counts visible first), and CTA 0's decision
             if (tid == 0) red_release_add(D.hcnt + HMAX, 1);
             // ---- wait for CTA 0's decision
             __shared__ int s_dec;
@@ -748,11 +1094,11 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             return !s_dec;  // undecided: the general step, from scratch
         }
     }
-    // ---- CTA 0: wait for every head cluster's rows and every row CTA, then certify
+    // ---- CTA 0: wait for every row CTA's arrival, then certify
     if (G > 1) {
-        for (int q = tid; q <= hn; q += THREADS) {
-            const int n = q < hn ? o.cum[q + 1] - o.cum[q] : G - 1;
-            const int *ctr = D.hcnt + (q < hn ? q : HMAX);
+        if (tid == 0) {
+            const int n = G - 1;
+            const int *ctr = D.hcnt + HMAX;
             unsigned long long spins = 0;
             int v;
             do {
@@ -782,7 +1128,11 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         D.dbg[61] = hn;
         D.dbg[62] = o.cum[hn];
     }
-    if (fits) {
+    const int fs = segs ? head_certify_seg(D, o, hn, Gr, (unsigned)epoch, s_est, hs, pw_hs_size(D.wplan), s_res) : -1;
+    if (lead && D.dbg) D.dbg[63] = (unsigned long long)(fs + 2);
+    if (fs >= 0) {
+        decided = fs != 0;
+    } else if (fits) {
         const int f = (o.cum[hn] <= 2 * THREADS * 8) ? head_certify_fast(D, o, hn, hs, s_res) : -1;
         if (lead && D.dbg) D.dbg[59] = (unsigned long long)(f + 2);
         decided = f < 0 ? head_certify(D, o, hn, hs, s_res) != 0 : f != 0;
@@ -814,7 +1164,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     }
     if (lead) DBG_TS(D, 31);
     // every row CTA has added its counts and arrived: reset
-    for (int q = tid; q <= HMAX; q += THREADS) D.hcnt[q] = 0;
+    for (int q = tid; q < HW_INTS; q += THREADS) D.hcnt[q] = 0;  // arrivals, histogram, candidate count
     if (tid == 0) {
         if (decided) {
             csvd_result r = s_res;
