@@ -444,7 +444,9 @@ static int configure(csvd_ctx *ctx) {
     // L2 bulk prefetch policy (measured: prefetching rows ahead in the dense GEMV
     // causes re-reads and costs 25%; CSVD_DENSE_PD / CSVD_PF override)
     D.dense_pd = getenv("CSVD_DENSE_PD") ? atoi(getenv("CSVD_DENSE_PD")) : 0;
-    D.pf_mask = getenv("CSVD_PF") ? atoi(getenv("CSVD_PF")) : 0;  // step: no measurable gain either way
+    // 4: the head step's row CTAs prefetch their W rows into L2 (measured no gain: off); 1 / 2: older
+    // prefetch points of the general step (no measurable gain either way)
+    D.pf_mask = getenv("CSVD_PF") ? atoi(getenv("CSVD_PF")) : 0;
     if (ctx->kdense) {
         ctx->dense_smem = sizeof(double) * (size_t)pw_hs_size(D.wplan);
         CK(cudaFuncSetAttribute((const void *)ctx->kdense, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -538,6 +538,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     // --- top cluster c0: argmin of (okey(U), id); every thread folds the warp results
     unsigned long long bk = ~0ull;
     int bi = 0x7fffffff;
+    #pragma unroll 1
     for (int c = tid; c < C; c += THREADS) {
         const unsigned long long k = okey(Us[c]);
         if (okey_before(k, c, bk, bi)) {
@@ -545,7 +546,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
             bi = c;
         }
     }
-#pragma unroll
+#pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, bk, off);
         const int i2 = __shfl_xor_sync(CSVD_FULL, bi, off);
@@ -560,7 +561,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     }
     if (tid == 0) s_n = 0;
     __syncthreads();
-#pragma unroll
+#pragma unroll 1
     for (int w = 0; w < WARPS; ++w)
         if (okey_before(s_k[w], s_i[w], bk, bi)) {
             bk = s_k[w];
@@ -574,6 +575,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     double xm = -INFINITY;
     bk = ~0ull;
     bi = 0x7fffffff;
+    #pragma unroll 1
     for (int c = tid; c < C; c += THREADS) {
         const double u = Us[c];
         xm = fmax(xm, xs[c]);
@@ -589,7 +591,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
         }
     }
     xm = warp_max(xm);
-#pragma unroll
+#pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const unsigned long long k2 = __shfl_xor_sync(CSVD_FULL, bk, off);
         const int i2 = __shfl_xor_sync(CSVD_FULL, bi, off);
@@ -609,11 +611,12 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 34);
     if (n > 64) return 0;
     double xmax = s_x[0];
-#pragma unroll
+#pragma unroll 1
     for (int w = 1; w < WARPS; ++w) xmax = fmax(xmax, s_x[w]);
     // --- residual mass of everything outside the head; the head's rank by
     // (key, id) among themselves (thread group of 4 per head element)
     double rest = 0.0;
+    #pragma unroll 1
     for (int c = tid; c < C; c += THREADS)
         if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, exp_nonpos(__dsub_rn(xs[c], xmax)));
     {
@@ -644,13 +647,13 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     __syncthreads();
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 35);
     double S_rest = 0.0;
-#pragma unroll
+#pragma unroll 1
     for (int w = 0; w < WARPS; ++w) S_rest = __dadd_rn(S_rest, s_x[w]);
     __shared__ int s_fail;
     if (warp == 0) {
         int cn = 0x7fffffff;
         unsigned long long kn = ~0ull;
-#pragma unroll
+#pragma unroll 1
         for (int w = 0; w < WARPS; ++w)
             if (okey_before(s_k[w], s_i[w], kn, cn)) {
                 kn = s_k[w];
@@ -661,7 +664,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
         const double ea = lane < n ? s_he[lane] : 0.0, eb = lane + 32 < n ? s_he[lane + 32] : 0.0;
         int ca = sa, cb = sb;  // inclusive prefix sums
         double ra = ea, rb = eb;  // inclusive suffix sums
-#pragma unroll
+#pragma unroll 1
         for (int off = 1; off < 32; off <<= 1) {
             const int ta = __shfl_up_sync(CSVD_FULL, ca, off), tb = __shfl_up_sync(CSVD_FULL, cb, off);
             const double ua = __shfl_down_sync(CSVD_FULL, ra, off), ub = __shfl_down_sync(CSVD_FULL, rb, off);

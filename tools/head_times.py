@@ -19,8 +19,8 @@ ctx = P.prepare(T, ix)
 lib = _lib.load()
 lib.csvd_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 cfg = P.DecodeConfig(k=10)
-names = {24: "kernel start", 63: "seg certifier used (+2)", 25: "h staged", 26: "cta0 bounds done", 27: "barrier passed", 28: "head done (cta0)",
-         29: "cta0: head rows complete", 31: "cta0: certified", 30: "decision published", 32: "stage_bounds", 33: "order: top cluster", 34: "order: membership", 35: "order: rest + rank", 55: "cert: cluster sums", 56: "cert: lane sorts", 58: "cert: kth merged", 52: "cert: staged + max", 53: "cert: clusters + top-k", 54: "cert: prefixes", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
+names = {24: "kernel start", 51: "cert warm-up done", 63: "seg certifier used (+2)", 25: "h staged", 26: "cta0 bounds done", 27: "barrier passed", 28: "head done (cta0)",
+         29: "cta0: head rows complete", 31: "cta0: certified", 30: "decision published", 32: "stage_bounds", 33: "order: top cluster", 34: "order: membership", 35: "order: rest + rank", 55: "cert: T (k-th segment max)", 56: "cert: candidates gathered", 58: "cert: k-th selected", 52: "cert: staged + max", 53: "cert: clusters + top-k", 54: "cert: prefixes", 40: "scan: min/max prefix", 41: "scan: log Z prefix",
          42: "scan: 64-merge recompute", 43: "scan: k-th merges", 44: "scan: rho/delta", 45: "scan: ballot+merge",
          46: "scan: state machine", 48: "summary: min/max", 49: "summary: warp min/max", 50: "summary: lse",
          51: "summary: sort"}
@@ -40,8 +40,8 @@ for i, h in enumerate(q):
     print(f"   rows done per CTA: first {rd.min() / 1e3:.2f} median {np.median(rd) / 1e3:.2f} "
           f"last {rd.max() / 1e3:.2f} us")
     print(f"   seg result {int(buf[63]) - 2} (1 decided, 0 general, -1 fallback)")
-    print(f"   calibration: 256 dependent DADD on CTA 0's SM took {int(buf[57])} cycles")
-    print(f"   certify path {int(buf[60])} (1 = block-parallel), fast result {int(buf[59]) - 2} "
+
+    print(f"   candidates / certify path {int(buf[60])} (1 = block-parallel), fast result {int(buf[59]) - 2} "
           f"(1 decided, 0 general, -1 full certifier), hn {int(buf[61])}, R {int(buf[62])}")
     sd = buf[128:128 + min(nb, 256)].astype(np.int64) - t0
     print(f"   decision seen per CTA: first {sd.min() / 1e3:.2f} median {np.median(sd) / 1e3:.2f} "
