@@ -9,14 +9,16 @@
 //   CTAs 1..G-1 (row CTAs): rows [b'*R/G', (b'+1)*R/G') of the head's opening
 //         order (contiguous, so a cluster spans 1-3 CTAs); bit-exact f64 logits
 //         go straight to S (and, for host-API steps, to the mapped host
-//         buffers); then one release-add per touched cluster  decode.py:169-176
-//   CTA 0 (the certifying CTA) does no rows: while they run it executes the
-//         summary and scan code once on scratch data (the code is cold after
-//         the L2 flush / the rest of a model, and a cold instruction stream
-//         costs more than the work), then its warps summarise each cluster as
-//         its counter completes (top-k values, log-sum-exp, min, max;
-//         certify.py:73-88) and warp 0 runs the certification scan
-//         (scan.cuh, decode.py:192-210), and publishes a decision word.
+//         buffers)                                             decode.py:169-176
+//         then the certification inputs of their own rows: a top-k histogram
+//         (integer counts, certify.py:128-139) and one record per (CTA,
+//         cluster) segment -- sum exp(S - est), min, max (certify.py:73-88) --
+//         and one release-add arrival
+//   CTA 0 (the certifying CTA) does no rows: it dry-runs the certifier while
+//         they run (its code is cold after the L2 flush / the rest of a
+//         model), waits for every arrival, reduces the records per cluster in
+//         a fixed order, tests every head prefix at once and publishes a
+//         decision word (head_certify_seg).
 //
 // Steps the head cannot decide (more than 64 head clusters, certification
 // past the head, the fallback chain, non-finite bounds) run the general step
