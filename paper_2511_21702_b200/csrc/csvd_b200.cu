@@ -641,7 +641,7 @@ static int ensure_lanes(csvd_ctx *ctx, int B) {
         CK(cudaMemset(L.bar64, 0, 32));
         L.nblocks = G;
         L.gsum = nullptr;  // distributed wave summaries: single-step contexts only
-        L.dbg = nullptr;
+        L.dbg = b == 0 ? D0.dbg : nullptr;  // debug timestamps follow lane 0
         L.res_host = nullptr;
         L.ids_host = nullptr;
         L.logits_host = nullptr;

@@ -982,7 +982,6 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         __syncthreads();
         return true;
     }
-    if (tid == 0) init_state(D, o, ss, hn, s_est);
     if (lead) DBG_TS(D, 28);
     const unsigned long long epoch = s_epoch;
     unsigned long long *decision = D.bar64 + 1;  // epoch * 2 + decided
@@ -1039,8 +1038,31 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             return lo;
         };
         const ET *Wt = reinterpret_cast<const ET *>(D.W);
+        // A warp with several row pairs (batch lanes: ~150 rows per warp)
+        // streams them with little in flight; its lane 0 keeps the rows of the
+        // pair PFD iterations ahead on their way to L2 (CSVD_PF bit 32: off)
+        constexpr int PFD = 3;
+        const size_t row_bytes = (size_t)D.d * sizeof(ET);
+        // rows of <= 8 KB only: larger rows put more ahead in flight than L2 keeps
+        // (c4, 32 KB f32 rows: 1.37 ms per batch against 1.27 ms without)
+        const bool pf_ahead = !(D.pf_mask & 32) && r_hi - r_lo > 4 * WARPS && row_bytes <= 8192;
+        auto prefetch_pair = [&](int r) {
+            if (r < r_hi) {
+                int w, pp;
+                locate(r, w, pp);
+                bulk_prefetch_l2(Wt + (size_t)w * D.d, row_bytes);
+            }
+            if (r + WARPS < r_hi) {
+                int w, pp;
+                locate(r + WARPS, w, pp);
+                bulk_prefetch_l2(Wt + (size_t)w * D.d, row_bytes);
+            }
+        };
+        if (pf_ahead && lane == 0)
+            for (int j = 0; j < PFD; ++j) prefetch_pair(r_lo + warp + j * 2 * WARPS);
 #pragma unroll 1
         for (int r = r_lo + warp; r < r_hi; r += 2 * WARPS) {
+            if (pf_ahead && lane == 0) prefetch_pair(r + PFD * 2 * WARPS);
             const int r2 = r + WARPS;
             int wa, pa, wb, pb, qb = 0;
             const int qa = locate(r, wa, pa);
@@ -1143,6 +1165,7 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     // ---- CTA 0: warm the certifier's code while the rows run (CSVD_PF bit 8
     // turns this off), then wait for every row CTA's arrival and certify
     __shared__ csvd_result s_res;
+    if (tid == 0) init_state(D, o, ss, hn, s_est);  // only the certifying CTA needs the scan state
     if (!cta0_rows && segs && !(D.pf_mask & 8)) {
         const SegArgs wa{D.hcnt, D.cfg, D.S_logits, nullptr, D.C};
         (void)head_certify_seg(wa, o, hn, Gr, 0xffffffffu, s_est, hs, pw_hs_size(D.wplan), &s_res, true);
@@ -1271,7 +1294,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_head_lanes(const __grid_constant
         D.logits_host = w.logits_host;
         D.hcnt = w.hcnt;
         D.bar64 = w.bar64;
-        D.dbg = nullptr;
+        D.dbg = blockIdx.x == 0 ? D0.dbg : nullptr;  // debug timestamps follow lane 0's CTA 0
     }
     __syncthreads();
     if (head_path<ET, Q, true>(D)) step_body<ET, 8, Q, 8, Q>(D);

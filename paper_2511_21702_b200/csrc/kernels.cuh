@@ -1898,15 +1898,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int gwarp = blockIdx.x * WARPS + warp, nwarps = gridDim.x * WARPS;
     if ((D.pf_mask & 1) && lane == 0)  // optional: this warp's centroid rows towards L2
         for (int c = gwarp; c < D.C; c += nwarps) bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
+    // Rounds of clusters (one warp task each: nwarps * NR clusters), each
+    // swept by every pass of queries before the next round: a round's
+    // centroid rows come from HBM once and from L2 for the other passes (a
+    // pass-major order re-streams all C rows per pass once C * d * 8 bytes
+    // outgrow the L2).  CSVD_PF bit 16 turns rounds on: measured no gain (c5
+    // B=128 2.26 ms against 2.19 ms pass-major; the kernel is f64-issue bound).
+    const bool rounds = (D.pf_mask & 16) != 0;
+    const int per_round = rounds ? nwarps * NR : D.C;
+    unsigned phase = 0;
+    for (int r0 = 0; r0 < D.C; r0 += per_round)
     for (int qb = 0; qb < B; qb += gq) {
         const int nq = min(gq, B - qb);
-        tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, (unsigned)(qb / gq));
+        const int r1 = min(D.C, r0 + per_round);
+        tma_stage_leaves(D.bplan, H + (size_t)qb * D.d, D.d, nq, smem, hs_stride, &s_bar, phase++);
         // one cluster per warp task (looping over the clusters), the
         // registers a second row would take hold more queries instead; the
         // row's next element step is in flight while the current one is used
         if constexpr (NR == 1) {
 #pragma unroll 1
-            for (int c = gwarp; c < D.C; c += nwarps) {
+            for (int c = r0 + gwarp; c < r1; c += nwarps) {
                 const double *const rows[1] = {D.cent + (size_t)c * D.bd};
                 double dots[1][BQN1];
                 warp_dot_regular_multi<BQ, BQN1, 1>(rows, smem, hs_stride, nq, D.bplan.leaf_len, lane, dots);
@@ -1918,8 +1929,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         } else {  // two clusters x BQN queries: every staged h value feeds both rows
 #pragma unroll 1
-            for (int c = gwarp; c < D.C; c += 2 * nwarps) {
-                const int c2 = c + nwarps < D.C ? c + nwarps : c;  // odd tail: recompute c, discard
+            for (int c = r0 + gwarp; c < r1; c += 2 * nwarps) {
+                const int c2 = c + nwarps < r1 ? c + nwarps : c;  // odd tail: recompute c, discard
                 const double *const rows[2] = {D.cent + (size_t)c * D.bd, D.cent + (size_t)c2 * D.bd};
 #pragma unroll 1
                 for (int j0 = 0; j0 < nq; j0 += BQN) {
