@@ -94,6 +94,12 @@ struct csvd_ctx {
     // head step (headstep.cuh): [h2d] -> k_head -> IF(undecided) k_step
     void (*khead)(Dev) = nullptr;
     cudaGraphExec_t g_step_head = nullptr, g_host_head = nullptr;
+    // the device head graph reads h where the caller keeps it: its kernel
+    // node's Dev.h is updated in the executable graph (a host-side call) when
+    // the caller's pointer changes, instead of a device-to-device copy node
+    cudaGraph_t g_step_head_src = nullptr;
+    cudaGraphNode_t g_step_head_node = nullptr;
+    const double *g_step_head_h = nullptr;
     // zero-copy host results (csvd_step_host): mapped pinned buffers + flag
     csvd_result *res_map = nullptr;
     long long *ids_map = nullptr;
@@ -518,9 +524,45 @@ static int capture_head(csvd_ctx *ctx, bool host_io, cudaGraphExec_t *out) {
         return fail(ctx, CSVD_ECUDA, std::string("head graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
     }
     e = cudaGraphInstantiate(out, g, 0);
+    if (e == cudaSuccess && !host_io) {  // keep the source graph: its kernel node addresses the exec's
+        size_t n = 1;
+        cudaGraphNode_t node = nullptr;
+        if (cudaGraphGetNodes(g, &node, &n) == cudaSuccess && n == 1) {
+            if (ctx->g_step_head_src) cudaGraphDestroy(ctx->g_step_head_src);
+            ctx->g_step_head_src = g;
+            ctx->g_step_head_node = node;
+            ctx->g_step_head_h = D.h;
+            return 0;
+        }
+    }
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(ctx, CSVD_ECUDA, std::string("head graph instantiate: ") + cudaGetErrorString(e));
     return 0;
+}
+
+static void drop_head_src(csvd_ctx *ctx) {
+    if (ctx->g_step_head_src) cudaGraphDestroy(ctx->g_step_head_src);
+    ctx->g_step_head_src = nullptr;
+    ctx->g_step_head_node = nullptr;
+    ctx->g_step_head_h = nullptr;
+}
+
+// Point the device head graph's kernel at h (no copy node); false: not possible
+static bool head_graph_set_h(csvd_ctx *ctx, const double *h) {
+    if (!ctx->g_step_head || !ctx->g_step_head_node) return false;
+    if (h == ctx->g_step_head_h) return true;
+    cudaKernelNodeParams kp{};
+    if (cudaGraphKernelNodeGetParams(ctx->g_step_head_node, &kp) != cudaSuccess || !kp.kernelParams) return false;
+    Dev D = *reinterpret_cast<Dev *>(kp.kernelParams[0]);
+    D.h = h;
+    void *args[] = {&D};
+    kp.kernelParams = args;
+    if (cudaGraphExecKernelNodeSetParams(ctx->g_step_head, ctx->g_step_head_node, &kp) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    ctx->g_step_head_h = h;
+    return true;
 }
 
 static int build_graphs(csvd_ctx *ctx) {
@@ -540,6 +582,7 @@ static int build_graphs(csvd_ctx *ctx) {
         if (*g) cudaGraphExecDestroy(*g);
         *g = nullptr;
     }
+    drop_head_src(ctx);
     int rc;
     if (ctx->D.W) {
         if ((rc = capture(ctx, LAUNCH_STEP, false, &ctx->g_step))) return rc;
@@ -948,6 +991,7 @@ extern "C" int csvd_reserve_k(csvd_ctx *ctx, int32_t k) {
             if (*g) cudaGraphExecDestroy(*g);
             *g = nullptr;
         }
+        drop_head_src(ctx);
         return rc;
     }
     return 0;
@@ -1196,6 +1240,7 @@ extern "C" int csvd_destroy(csvd_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (cudaGraphExec_t g : {ctx->g_step, ctx->g_host, ctx->g_bounds, ctx->g_dense, ctx->g_step_head, ctx->g_host_head})
         if (g) cudaGraphExecDestroy(g);
+    drop_head_src(ctx);
     free_lanes(ctx);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     for (void *p : ctx->dev_allocs) cudaFree(p);
@@ -1262,11 +1307,17 @@ extern "C" int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_c
     CK(cudaSetDevice(ctx->device));
     int rc = check_cfg(ctx, cfg);
     if (rc) return rc;
-    if (h_dev && h_dev != ctx->d_h)
-        CK(cudaMemcpyAsync(ctx->d_h, h_dev, sizeof(double) * ctx->D.d, cudaMemcpyDeviceToDevice, s));
+    const bool head = !ctx->direct && ctx->g_step_head && head_config(cfg);
+    const double *hsrc = h_dev ? h_dev : ctx->d_h;
+    const bool in_place = head && ((uintptr_t)hsrc % 16 == 0) && head_graph_set_h(ctx, hsrc);
+    if (!in_place) {
+        if (head && !head_graph_set_h(ctx, ctx->d_h)) return fail(ctx, CSVD_ECUDA, "head graph: cannot reset h");
+        if (h_dev && h_dev != ctx->d_h)
+            CK(cudaMemcpyAsync(ctx->d_h, h_dev, sizeof(double) * ctx->D.d, cudaMemcpyDeviceToDevice, s));
+    }
     if ((rc = sync_cfg(ctx, cfg, s))) return rc;
     if (ctx->direct) return launch(ctx, LAUNCH_STEP, s);
-    cudaGraphExec_t g = (ctx->g_step_head && head_config(cfg)) ? ctx->g_step_head : ctx->g_step;
+    cudaGraphExec_t g = head ? ctx->g_step_head : ctx->g_step;
     if (!g) return fail(ctx, CSVD_ESTATE, "no step graph (an earlier workspace change failed)");
     CK(cudaGraphLaunch(g, s));
     ctx->last_launches = 1;  // one step kernel (it runs the fallback chain itself)

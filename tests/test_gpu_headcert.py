@@ -88,3 +88,47 @@ def test_head_duplicate_logits_kth(case):
             exp = O.decode_step(T2, ix2, h, cfg)
             got = P.decode_step(T2, ix2, h, cfg)
             assert_outcome(got, _fields(exp), rtol=TRANS_RTOL, where=f"dup k={k},{i}")
+
+
+def test_device_step_reads_h_in_place(case):
+    """csvd_step_device with caller-owned device queries (the head graph's
+    kernel reads h where it lies, re-pointed per call): outcomes equal the
+    host API's, whichever buffer each step's h comes from."""
+    import ctypes
+
+    import torch
+    from paper_2511_21702_b200 import _lib
+    T, ix, q = case
+    ctx = P.prepare(T, ix)
+    lib = _lib.load()
+    cfg = P.DecodeConfig(k=10, epsilon=0.05)
+    ccfg = ctx.make_config(cfg)
+    hq = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    ids_p, log_p, res_p = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    lib.csvd_outputs(ctx._ctx, ctypes.byref(ids_p), ctypes.byref(log_p), ctypes.byref(res_p))
+    sp = ctypes.c_void_p()
+    lib.csvd_stream(ctx._ctx, ctypes.byref(sp))
+    for rep in range(2):
+        for i in [0, 1, 2, 1, 0, 3, 3]:
+            h = hq[i] if rep == 0 else hq[i].clone()  # the same pointers again / fresh buffers
+            assert lib.csvd_step_device(ctx._ctx, h.data_ptr(), ctypes.byref(ccfg), sp) == 0
+            torch.cuda.synchronize()
+            exp = P.decode_step(T, ix, q[i], cfg)
+            n = exp.stats.sub_size
+            r = _lib.Result()
+            ctypes.memmove(ctypes.byref(r), _d2h(res_p.value, ctypes.sizeof(_lib.Result), np.uint8).ctypes.data,
+                           ctypes.sizeof(_lib.Result))
+            assert int(r.sub_size) == n, (rep, i)
+            assert np.array_equal(_d2h(ids_p.value, n, np.int64), exp.token_ids), (rep, i)
+            assert np.array_equal(_d2h(log_p.value, n, np.float64).view(np.int64), exp.logits.view(np.int64)), (rep, i)
+
+
+def _d2h(ptr, n, dtype):
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:  # older cuda-python layout
+        from cuda import cudart as rt
+    out = np.empty(n, dtype=dtype)
+    err, = rt.cudaMemcpy(out.ctypes.data, ptr, out.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    assert int(err) == 0, err
+    return out
