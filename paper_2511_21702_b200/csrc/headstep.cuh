@@ -680,10 +680,30 @@ static __device__ __noinline__ int head_certify_seg(const SegArgs D, const Ord o
     __shared__ int s_hist[HMAX + 2];
     __shared__ int s_p, s_kind, s_tie, s_nc, s_cnt[HMAX + 1];
     __shared__ double s_T;
+    if (scratch_n < THREADS + 64) return -1;  // (tiny d) no room for the candidates
+    const int nslots = Gr + hn;
+    double *sm = scratch, *cl = scratch + THREADS;  // segment maxima by slot | candidates
+    int cap = 2048;  // a power of two: the bitonic sort below pads to one
+    while (cap > scratch_n - THREADS) cap >>= 1;
+    __shared__ int s_sq[HW_SEGS];                   // segment cluster positions by slot
     if (tid <= hn) s_hist[tid] = __ldcg(D.hcnt + HW_HIST + tid);
     if (tid == 0) {
         s_nc = 0;
         s_T = -INFINITY;
+    }
+    {  // every segment's maximum, for the k-th threshold below (same round trip as the records)
+        double m = -INFINITY;
+        int sq = 0x7fffffff;
+        if (tid < nslots) {
+            const double2 c = __ldcg(reinterpret_cast<const double2 *>(rec + tid) + 1);
+            const unsigned long long tag = (unsigned long long)__double_as_longlong(c.y);
+            if ((unsigned)(tag >> 32) == ep) {
+                m = c.x;
+                sq = (int)(unsigned)tag;
+            }
+        }
+        sm[tid] = m;
+        s_sq[tid] = sq;
     }
     // per cluster q (warp q % WARPS): its records sit in slots q + b, b < Gr
 #pragma unroll 1
@@ -724,6 +744,41 @@ static __device__ __noinline__ int head_certify_seg(const SegArgs D, const Ord o
     }
     __syncthreads();
     if (DBG_HERE(D) && tid == 0) DBG_TS(D, 53);
+    // While warp 0 tests the prefixes, warps 1..7 prepare the k-th logit of
+    // the whole head (the usual decision prefix ps = hn): T = the k-th largest
+    // segment maximum (at least k logits reach it, so the k-th logit does
+    // too), then the head's logits at or above T.
+    const int R = o.cum[hn];
+    const bool spec = R >= k && nslots <= THREADS - 32;
+    if (warp > 0 && spec) {
+        const int t = tid - 32;
+        if (t < nslots) {
+            const double m = sm[t];
+            if (m != -INFINITY) {
+                int rank = 0;
+#pragma unroll 4
+                for (int j = 0; j < nslots; ++j) {
+                    const double w = sm[j];
+                    rank += (w > m || (w == m && j < t)) ? 1 : 0;
+                }
+                if (rank == k - 1) s_T = m;
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(THREADS - 32) : "memory");
+        const double T = s_T;
+#pragma unroll 1
+        for (int i0 = t; i0 < R; i0 += 8 * (THREADS - 32)) {
+            double x[8];  // eight loads in flight
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = __ldcg(D.S_logits + min(i0 + j * (THREADS - 32), R - 1));
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j)
+                if (i0 + j * (THREADS - 32) < R && x[j] >= T) {
+                    const int slot = atomicAdd(&s_nc, 1);
+                    if (slot < cap) cl[slot] = x[j];
+                }
+        }
+    }
     // ---- every prefix at once (warp 0: lane l tests p = l + 1 and l + 33)
     if (warp == 0) {
         int carry = 0;
@@ -783,51 +838,41 @@ static __device__ __noinline__ int head_certify_seg(const SegArgs D, const Ord o
     if (ps > hn || kind == 99) return 0;
     const int n = o.cum[ps];
     double kth = -INFINITY;
-    if (n >= k && scratch_n < THREADS + 64) return -1;
     if (n >= k) {
-        // T = the k-th largest maximum among the segments of clusters < ps
-        // (slot s = b + q, at most Gr + hn <= HW_SEGS <= THREADS of them)
-        double *sm = scratch, *cl = scratch + THREADS;
-        const int cap = min(2048, scratch_n - THREADS);
-        // when at most THREADS logits exceed Uo[ps] and at least k do (a top-k
-        // certificate), those are the candidates: no T needed
-        const int cps = s_cnt[ps];
-        const bool direct = !warm && ps < D.C && cps >= k && cps <= THREADS;
-        double m = -INFINITY;
-        if (!direct && tid < Gr + hn) {
-            const double2 c = __ldcg(reinterpret_cast<const double2 *>(rec + tid) + 1);
-            const unsigned long long tag = (unsigned long long)__double_as_longlong(c.y);
-            if ((unsigned)(tag >> 32) == ep && (int)(unsigned)tag < ps) m = c.x;
-        }
-        sm[tid] = m;
-        __syncthreads();
-        if (!direct && m != -INFINITY) {
-            int rank = 0;
-#pragma unroll 4
-            for (int j = 0; j < Gr + hn; ++j) {
-                const double w = sm[j];
-                rank += (w > m || (w == m && j < tid)) ? 1 : 0;
+        if (!(spec && ps == hn)) {
+            // an earlier decision prefix: T and the candidates over its clusters only
+            if (tid == 0) {
+                s_nc = 0;
+                s_T = -INFINITY;
             }
-            if (rank == k - 1) s_T = m;
-        }
-        __syncthreads();
-        if (DBG_HERE(D) && tid == 0) DBG_TS(D, 55);
-        // candidates: the first n logits at or above T (at least k of them)
-        const double T = direct ? o.Uo[ps] : s_T;
-#pragma unroll 1
-        for (int i0 = tid; i0 < n; i0 += 8 * THREADS) {
-            double x[8];  // eight loads in flight
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = __ldcg(D.S_logits + min(i0 + j * THREADS, n - 1));
-#pragma unroll 1
-            for (int j = 0; j < 8; ++j)
-                if (i0 + j * THREADS < n && (x[j] > T || (!direct && x[j] == T))) {
-                    const int slot = atomicAdd(&s_nc, 1);
-                    if (slot < cap) cl[slot] = x[j];
+            __syncthreads();
+            const double m = (tid < nslots && s_sq[tid] < ps) ? sm[tid] : -INFINITY;
+            if (m != -INFINITY) {
+                int rank = 0;
+#pragma unroll 4
+                for (int j = 0; j < nslots; ++j) {
+                    const double w = (s_sq[j] < ps) ? sm[j] : -INFINITY;
+                    rank += (w > m || (w == m && j < tid)) ? 1 : 0;
                 }
+                if (rank == k - 1) s_T = m;
+            }
+            __syncthreads();
+            const double T = s_T;
+#pragma unroll 1
+            for (int i0 = tid; i0 < n; i0 += 8 * THREADS) {
+                double x[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[j] = __ldcg(D.S_logits + min(i0 + j * THREADS, n - 1));
+#pragma unroll 1
+                for (int j = 0; j < 8; ++j)
+                    if (i0 + j * THREADS < n && x[j] >= T) {
+                        const int slot = atomicAdd(&s_nc, 1);
+                        if (slot < cap) cl[slot] = x[j];
+                    }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        const int nc = s_nc;
+        const int nc = warm ? min(s_nc, THREADS) : s_nc;  // a dry run stays inside the buffers
         if (DBG_HERE(D) && tid == 0) DBG_TS(D, 56);
         if (!warm && (nc > cap || nc < k)) return -1;
         if (nc <= THREADS) {  // one candidate per thread: its rank by counting
@@ -947,6 +992,14 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         }
     }
     __syncthreads();
+    if constexpr (!GROUPED) {  // CSVD_PF bit 64: this warp's centroid rows stream to L2 while h is staged
+        // (measured: h staging slows from 1.5 to 3.7 us and the step does not gain; off)
+        if ((D.pf_mask & 64) && lane == 0) {
+            int j = 0;
+            for (int c = warp * G + b; c < D.C && j < MAX_PER_WARP; c += G * WARPS, ++j)
+                bulk_prefetch_l2(D.cent + (size_t)c * D.bd, sizeof(double) * D.bd);
+        }
+    }
     tma_stage_leaves(D.wplan, D.h, D.d, 1, hs, 0, &s_hbar, 0);
     if (b == 1 % G && warp == 0 && lane == 0) {  // per-cluster arrays the head and rows read next
         bulk_prefetch_l2(D.logsz, sizeof(double) * D.C);
@@ -1233,8 +1286,16 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
         __syncthreads();
     }
     if (lead) DBG_TS(D, 31);
+    if (tid == 0) {
+        // the decision first: the row CTAs only need this word (and exit or
+        // start the general step); the result below is read after the kernel
+        if constexpr (GROUPED) D.bar64[0] = epoch;  // the lane's step count (read before the next step)
+        const unsigned long long w = epoch * 2 + (decided ? 1 : 0);
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(decision), "l"(w) : "memory");
+        DBG_TS(D, 30);
+    }
     // every row CTA has added its counts and arrived: reset
-    for (int q = tid; q < HW_INTS; q += THREADS) D.hcnt[q] = 0;  // arrivals, histogram, candidate count
+    for (int q = tid; q < HW_INTS; q += THREADS) D.hcnt[q] = 0;  // arrivals, histogram
     if (tid == 0) {
         if (decided) {
             csvd_result r = s_res;
@@ -1251,10 +1312,6 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             *D.st = s2;
             if (D.res_host) *D.res_host = r;
         }
-        if constexpr (GROUPED) D.bar64[0] = epoch;  // the lane's step count (read before the next step)
-        const unsigned long long w = epoch * 2 + (decided ? 1 : 0);
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(decision), "l"(w) : "memory");
-        DBG_TS(D, 30);
     }
     __syncthreads();
     return !decided;

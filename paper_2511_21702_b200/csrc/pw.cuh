@@ -238,7 +238,10 @@ template <typename ET, int Q>
 __device__ __forceinline__ void warp_dot_r8_x2(const ET *__restrict__ rowA, const ET *__restrict__ rowB,
                                                const double *__restrict__ hs, int leaf_len, int lane, double &outA,
                                                double &outB) {
-    constexpr int NB = NBatch<ET, 8>::value / 4;  // loads per row per buffer
+#ifndef CSVD_X2_DIV
+#define CSVD_X2_DIV 4  // 2 (twice the loads in flight, 240 registers) measured no faster
+#endif
+    constexpr int NB = NBatch<ET, 8>::value / CSVD_X2_DIV;  // loads per row per buffer
     const int S = leaf_len >> 3;
     double slA[Q], slB[Q];
 #pragma unroll
