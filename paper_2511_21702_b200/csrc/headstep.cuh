@@ -780,34 +780,60 @@ static __device__ __noinline__ int head_certify_seg(const SegArgs D, const Ord o
         }
     }
     // ---- every prefix at once (warp 0: lane l tests p = l + 1 and l + 33)
+    // every lane also finishes its prefix's outcome values (rho, xi,
+    // epsilon_achieved) should it be the decision: no serial tail afterwards
+    __shared__ double s_prho[HMAX + 1], s_pxi[HMAX + 1], s_peps[HMAX + 1];
     if (warp == 0) {
         int carry = 0;
-        double zc = 0.0;
+        double zc = 0.0, loc = INFINITY, hic = -INFINITY;
         int first = 0x7fffffff, kind = -1, tie_p = 0x7fffffff, bad = 0;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int p = lane + 1 + 32 * h;
             int c = p <= hn ? s_hist[p] : 0;
             double z = p <= hn ? s_zq[p - 1] : 0.0;
+            double lo = p <= hn ? s_mnq[p - 1] : INFINITY, hi = p <= hn ? s_mxq[p - 1] : -INFINITY;
 #pragma unroll 1
             for (int off = 1; off < 32; off <<= 1) {
                 const int u = __shfl_up_sync(CSVD_FULL, c, off);
                 const double w = __shfl_up_sync(CSVD_FULL, z, off);
+                const double wl = __shfl_up_sync(CSVD_FULL, lo, off), wh = __shfl_up_sync(CSVD_FULL, hi, off);
                 if (lane >= off) {
                     c += u;
                     z = __dadd_rn(z, w);
+                    lo = fmin(lo, wl);
+                    hi = fmax(hi, wh);
                 }
             }
             c += carry;
             z = __dadd_rn(z, zc);
+            lo = fmin(lo, loc);
+            hi = fmax(hi, hic);
             carry = __shfl_sync(CSVD_FULL, c, 31);
             zc = __shfl_sync(CSVD_FULL, z, 31);
+            loc = __shfl_sync(CSVD_FULL, lo, 31);
+            hic = __shfl_sync(CSVD_FULL, hi, 31);
             if (p <= hn) {
                 s_zq[p - 1] = z;  // now Z(p)
                 s_cnt[p] = c;     // #{logits of the first p clusters > Uo[p]}
                 bad |= !(z > 1e-290 && z < 1e290);
                 int tie;
-                const int kd = seg_prefix_kind(D.cfg, D.C, p, o.cum[p], c, __dadd_rn(est, csvd_log(z)), o.lrh[p], &tie);
+                const double lz = __dadd_rn(est, csvd_log(z)), lr = o.lrh[p];
+                const int kd = seg_prefix_kind(D.cfg, D.C, p, o.cum[p], c, lz, lr, &tie);
+                // certify.py:93-107 and decode.py:212-237 for this prefix
+                const double rho = csvd_rho(lz, lr);
+                const double um = p >= D.C ? -INFINITY : o.Uo[p];
+                const int np = o.cum[p];
+                s_prho[p] = rho;
+                s_pxi[p] = (np < 2 || p >= D.C) ? NAN : (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
+                double eps_ach = 0.0;
+                if (kd == CSVD_KIND_SOFTMAX_EPS) {
+                    eps_ach = rho;
+                } else if (kd == CSVD_KIND_TOPP_MASS) {
+                    const double dl = csvd_delta(lz, lr);
+                    eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
+                }
+                s_peps[p] = eps_ach;
                 if (kd >= 0 && p < first) {
                     first = p;
                     kind = kd;
@@ -917,49 +943,19 @@ static __device__ __noinline__ int head_certify_seg(const SegArgs D, const Ord o
             D.dbg[60] = nc;
         }
     }
-    if (warp == 0) {
-        double lo = INFINITY, hi = -INFINITY;
-        if (lane < ps) {
-            lo = s_mnq[lane];
-            hi = s_mxq[lane];
-        }
-        if (lane + 32 < ps) {
-            lo = fmin(lo, s_mnq[lane + 32]);
-            hi = fmax(hi, s_mxq[lane + 32]);
-        }
-#pragma unroll 1
-        for (int off = 16; off; off >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(CSVD_FULL, lo, off));
-            hi = fmax(hi, __shfl_xor_sync(CSVD_FULL, hi, off));
-        }
-        if (lane == 0) {
-            const double lz = __dadd_rn(est, csvd_log(s_zq[ps - 1]));
-            const double lr = o.lrh[ps];
-            const double rho = csvd_rho(lz, lr);
-            const double um = ps >= D.C ? -INFINITY : o.Uo[ps];
-            double xi;
-            if (n < 2 || ps >= D.C) xi = NAN;
-            else xi = (um <= lo) ? 1.0 : csvd_ddiv(__dsub_rn(hi, lo), __dsub_rn(um, lo));
-            double eps_ach = 0.0;
-            if (kind == CSVD_KIND_SOFTMAX_EPS) {
-                eps_ach = rho;
-            } else if (kind == CSVD_KIND_TOPP_MASS) {
-                const double dl = csvd_delta(lz, lr);
-                eps_ach = isfinite(dl) ? csvd_ddiv(dl, __dadd_rn(1.0, dl)) : 1.0;
-            }
-            memset(&res, 0, sizeof(res));
-            res.kind = kind;
-            res.fallback = CSVD_FB_NONE;
-            res.sub_size = n;
-            res.clusters_opened = ps;
-            res.heap_pops = ps;
-            res.epsilon_achieved = eps_ach;
-            res.u_max = um;
-            res.topk_min = kth;
-            res.rho = rho;
-            res.xi = xi;
-            res.flags = s_tie ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
-        }
+    if (tid == 0) {
+        memset(&res, 0, sizeof(res));
+        res.kind = kind;
+        res.fallback = CSVD_FB_NONE;
+        res.sub_size = n;
+        res.clusters_opened = ps;
+        res.heap_pops = ps;
+        res.epsilon_achieved = s_peps[ps];
+        res.u_max = ps >= D.C ? -INFINITY : o.Uo[ps];
+        res.topk_min = kth;
+        res.rho = s_prho[ps];
+        res.xi = s_pxi[ps];
+        res.flags = s_tie ? CSVD_FLAG_TIE_AMBIGUOUS : 0;
     }
     __syncthreads();
     return 1;
