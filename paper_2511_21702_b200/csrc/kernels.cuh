@@ -481,11 +481,30 @@ static __device__ __forceinline__ bool stage_bounds(const Dev &D, const Ord &o, 
     if (!D.pre_bounds) {
 #pragma unroll 4
         for (int c = tid; c < C; c += THREADS) put(c, __ldcg(D.Uraw + c), __ldcg(D.dots + c));
-    } else {  // batched bounds: U from the given dots (bounds.py:79-83 / 95-118) and this lane's ||h||
+    } else if (D.mode != CSVD_MODE_SPHERICAL) {
+        // batched bounds: U from the given dots (bounds.py:79-83) and this
+        // lane's ||h||; four clusters' loads in flight per thread (a lane of
+        // one CTA walks every cluster: C / 256 dependent L2 round trips otherwise)
+#pragma unroll 1
+        for (int c0 = tid; c0 < C; c0 += 4 * THREADS) {
+            double dt[4], rr[4], mb[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = min(c0 + j * THREADS, C - 1);
+                dt[j] = __ldcg(D.dots + c);
+                rr[j] = __ldg(D.radii + c);
+                mb[j] = __ldg(D.maxb + c);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c0 + j * THREADS < C)
+                    put(c0 + j * THREADS, __dadd_rn(__dadd_rn(dt[j], __dmul_rn(rr[j], qn_given)), mb[j]), dt[j]);
+        }
+    } else {  // spherical (bounds.py:95-118)
 #pragma unroll 1
         for (int c = tid; c < C; c += THREADS) {
             const double dt = __ldcg(D.dots + c);
-            put(c, bound_from_dot(D, c, dt, qn_given), dt);
+            put(c, cone_bound(D, c, dt, qn_given), dt);
         }
     }
     double eta = 0.0;
