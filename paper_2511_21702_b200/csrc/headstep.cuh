@@ -1120,17 +1120,20 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
                 wb = wa;
                 pb = pa;
             }
+            // bias and token id first: their loads wait alongside the row's
+            const double ba = __ldg(D.bias + pa), bb = __ldg(D.bias + pb);
+            const int ia = __ldg(D.perm + pa), ib = __ldg(D.perm + pb);
             double la, lb;
             warp_dot_r8_x2<ET, Q>(Wt + (size_t)wa * D.d, Wt + (size_t)wb * D.d, hs, D.wplan.leaf_len, lane, la, lb);
             if (lane == 0) {
-                const double xa = __dadd_rn(la, __ldg(D.bias + pa));
+                const double xa = __dadd_rn(la, ba);
                 D.S_logits[r] = xa;
-                D.S_ids[r] = __ldg(D.perm + pa);
+                D.S_ids[r] = ia;
                 if (segs) tally(xa, qa);
                 if (r2 < r_hi) {
-                    const double xb = __dadd_rn(lb, __ldg(D.bias + pb));
+                    const double xb = __dadd_rn(lb, bb);
                     D.S_logits[r2] = xb;
-                    D.S_ids[r2] = __ldg(D.perm + pb);
+                    D.S_ids[r2] = ib;
                     if (segs) tally(xb, qb);
                 }
             }
