@@ -209,7 +209,11 @@ int csvd_step_host(csvd_ctx *ctx, const double *h, const csvd_config *cfg,
 
 /* Device-resident variant: h_dev is a device pointer to d doubles (the
  * bias-augmented [h, 1] is formed on the device), nothing is copied back; read
- * results with csvd_outputs().  Asynchronous on `stream`. */
+ * results with csvd_outputs().  Asynchronous on `stream`.  For head-eligible
+ * configs the step kernel reads h_dev in place (16-byte aligned pointers; the
+ * graph's kernel node is re-pointed on the host when h_dev changes), so the
+ * buffer must hold h until the step has run in stream order, as for any
+ * kernel input; otherwise h is first copied into the context's own buffer. */
 int csvd_step_device(csvd_ctx *ctx, const double *h_dev, const csvd_config *cfg,
                      void *stream);
 int csvd_outputs(csvd_ctx *ctx, int64_t **ids_dev, double **logits_dev,
