@@ -1026,7 +1026,11 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     __shared__ double s_slack, s_est;
     const bool ok = stage_bounds(D, o, qn, &s_slack);
     if (lead) DBG_TS(D, 32);
-    const int hn = ok ? order_head(D, o, s_est) : 0;
+    // row CTAs skip log R-hat (only the certifier reads it); a residual too
+    // small for the direct form is then seen by CTA 0 alone, which declares
+    // the step undecided once the rows are in (hfail)
+    int hfail = 0;
+    const int hn = ok ? order_head(D, o, s_est, b == 0, &hfail) : 0;
     if (hn == 0) {  // every CTA sees the same: the general step decides
         __syncthreads();
         return true;
@@ -1214,11 +1218,13 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
             return !s_dec;  // undecided: the general step, from scratch
         }
     }
-    // ---- CTA 0: warm the certifier's code while the rows run (CSVD_PF bit 8
-    // turns this off), then wait for every row CTA's arrival and certify
+    // ---- CTA 0: optionally (CSVD_PF bit 8) warm the certifier's code while the
+    // rows run -- ~1 us faster while CTA 0 also built log R-hat ahead of the
+    // rows, on the critical path (+1 us) since the row CTAs skip it -- then
+    // wait for every row CTA's arrival and certify
     __shared__ csvd_result s_res;
     if (tid == 0) init_state(D, o, ss, hn, s_est);  // only the certifying CTA needs the scan state
-    if (!cta0_rows && segs && !(D.pf_mask & 8)) {
+    if (!cta0_rows && segs && !hfail && (D.pf_mask & 8)) {
         const SegArgs wa{D.hcnt, D.cfg, D.S_logits, nullptr, D.C};
         (void)head_certify_seg(wa, o, hn, Gr, 0xffffffffu, s_est, hs, pw_hs_size(D.wplan), &s_res, true);
         if (lead) DBG_TS(D, 51);
@@ -1244,8 +1250,9 @@ __device__ __forceinline__ bool head_path(const Dev &D) {
     bool decided;
     const bool fits = head_fits(D, o, hn) && D.cfg->k <= KH;
     const SegArgs sa{D.hcnt, D.cfg, D.S_logits, DBG_HERE(D) ? D.dbg : nullptr, D.C};
-    const int fs = segs ? head_certify_seg(sa, o, hn, Gr, (unsigned)epoch, s_est, hs, pw_hs_size(D.wplan), &s_res, false)
-                        : -1;
+    const int fs = hfail ? 0
+                   : segs ? head_certify_seg(sa, o, hn, Gr, (unsigned)epoch, s_est, hs, pw_hs_size(D.wplan), &s_res, false)
+                          : -1;
     if (lead && D.dbg) {
         if (fs < 0) D.dbg[60] = fits ? 1 : 2;
         D.dbg[61] = hn;

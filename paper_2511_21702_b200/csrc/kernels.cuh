@@ -544,7 +544,11 @@ __device__ __forceinline__ bool okey_before(unsigned long long ka, int ia, unsig
 // p = n needs).  Returns n, or 0 when the head does not apply (more than 64
 // clusters, or a residual sum too small for the direct form): then the full
 // sort runs instead.
-static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, double &est_out) {
+// lrh = false (the head step's row CTAs): no log R-hat (and no underflow test,
+// fail_out = 0): only the certifying CTA reads them.  fail_out: report the
+// residual-underflow case there instead of returning 0.
+static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, double &est_out, bool lrh = true,
+                                                 int *fail_out = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = D.C;
     const double *__restrict__ Us = o.Us;
@@ -636,7 +640,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
     // (key, id) among themselves (thread group of 4 per head element)
     double rest = 0.0;
     #pragma unroll 1
-    for (int c = tid; c < C; c += THREADS)
+    for (int c = lrh ? tid : C; c < C; c += THREADS)
         if (!(Us[c] >= est || c == c0)) rest = __dadd_rn(rest, exp_nonpos(__dsub_rn(xs[c], xmax)));
     {
         const int e = tid >> 2, part = tid & 3;
@@ -657,7 +661,7 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
             s_hc[rank] = ie;
             s_hu[rank] = Us[ie];
             s_hz[rank] = o.cum[ie];  // |c| by id (stage_bounds)
-            s_he[rank] = exp_nonpos(__dsub_rn(xs[ie], xmax));
+            s_he[rank] = lrh ? exp_nonpos(__dsub_rn(xs[ie], xmax)) : 0.0;
         }
     }
     rest = warp_sum(rest);
@@ -721,15 +725,22 @@ static __device__ __forceinline__ int order_head(const Dev &D, const Ord &o, dou
                 fail |= !(S_rest > 1e-280);
             }
         }
-        // log R-hat after every head prefix (two logs per lane, independent)
-        const double la = lane < n ? csvd_log(ta) : 0.0, lb = lane + 32 < n ? csvd_log(tb) : 0.0;
-        if (lane < n) o.lrh[lane] = __dadd_rn(xmax, la);
-        if (lane + 32 < n) o.lrh[lane + 32] = __dadd_rn(xmax, lb);
-        if (lane == 0) o.lrh[n] = n < C ? __dadd_rn(xmax, csvd_log(S_rest)) : -INFINITY;
+        if (lrh) {  // log R-hat after every head prefix (two logs per lane, independent)
+            const double la = lane < n ? csvd_log(ta) : 0.0, lb = lane + 32 < n ? csvd_log(tb) : 0.0;
+            if (lane < n) o.lrh[lane] = __dadd_rn(xmax, la);
+            if (lane + 32 < n) o.lrh[lane + 32] = __dadd_rn(xmax, lb);
+            if (lane == 0) o.lrh[n] = n < C ? __dadd_rn(xmax, csvd_log(S_rest)) : -INFINITY;
+        } else {
+            fail = 0;
+        }
         fail = __any_sync(CSVD_FULL, fail);
         if (lane == 0) s_fail = fail;
     }
     __syncthreads();
+    if (fail_out) {
+        *fail_out = s_fail;
+        return n;
+    }
     return s_fail ? 0 : n;
 }
 
