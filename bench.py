@@ -72,7 +72,8 @@ def parse():
 
 
 def workload_name(a):
-    return f"llama3-8b-head V={a.V} d={a.d} C={a.C} g={a.g} {a.dtype} B=1"
+    name = "llama3-8b-head" if (a.V, a.d) == (128256, 4096) else "synthetic-head"  # c1: V=32000
+    return f"{name} V={a.V} d={a.d} C={a.C} g={a.g} {a.dtype} B=1"
 
 
 def c2_config(a, world=1):
